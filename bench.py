@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark: the paper's Euler-Newton step on a batch of cyclic-10 points.
+
+One "step" = one pht_pc_step over the whole per-GPU batch: every point gets an Euler
+prediction and one Newton correction, i.e. 2 fused (evaluate H, dH/dx, dH/dt -> 2-RHS
+direction solve -> update) passes = all rows a1..a6 of SURVEY §8(a).  Workload =
+BASELINE.json configs[2] (cyclic-10, "batched evaluation and predictor-corrector"),
+synthetic seeded points, 2^22 points per GPU (weak scaling, paths are
+independent: no collective in the data path, ledger R20).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (oracle/) on a
+bounded sample of the same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H+Jacobian evals/sec and paths tracked/sec (fp64) at 1/2/4/8 B200"
+UNIT = "evals/s"
+N_VARS = 10
+LIFT_MAX = 100
+DTAU = 1e-3
+TAU_LO = -0.05  # points with well-conditioned Jacobians
+
+
+def _system():
+    import workloads as W
+    return W.cyclic(N_VARS, lift_max=LIFT_MAX)
+
+
+def algorithmic_flops_per_eval(sysm) -> dict:
+    """FP64 flops one evaluation + direction solve needs (FMA = 2 flops).
+
+    Stage 2 is counted sparse (only nonzero exponents), stage 3 at the table-driven exp*cis
+    cost (11 + 16 + 2 ops of which 22 are FMAs -> 51 flops), stage 4 sparse; stage 1 per
+    variable (log 0.5*log|x|^2 + atan2 + reciprocal) at 80 flops; the solve is complex LU with
+    two right-hand sides (8 n^3/3 + 16 n^2 real flops) plus the x (.) delta update (6 n).
+    """
+    n, M = sysm.n, sysm.M
+    nnz = int(np.count_nonzero(sysm.exps))
+    stage2 = 2 * nnz + 2 * M + 2 * nnz        # phi (nnz FMA + omega tau), theta (nnz FMA)
+    stage2 += 2 * nnz + 2 * M                 # row-max pass (phi again)
+    stage3 = 51 * M + 4 * M                   # exp*cis, y = phi - e ln2 (2 FMA)
+    stage4 = 2 * M + 4 * nnz + 4 * M          # h, G_j (complex += real*complex), G_tau
+    stage1 = 80 * n
+    solve = 8 * n ** 3 / 3 + 16 * n ** 2 + 6 * n
+    return dict(eval=stage1 + stage2 + stage3 + stage4, solve=solve,
+                total=stage1 + stage2 + stage3 + stage4 + solve)
+
+
+def fp64_peak_tflops(sm_mhz: float) -> float:
+    """148 SMs x 64 FP64 FMA/clk x 2 flops x clock (B200_PROFILING.md unit counts)."""
+    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons DURING the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return None
+        try:
+            sm = [float(s[0]) for s in self.samples]
+            mx = float(self.samples[0][1])
+        except Exception:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """The oracle (oracle/), as it stands, on this host's cores, on a bounded sample."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    sysm = _system()
+    o = oracle.Oracle(sysm)
+    cores = oracle.set_threads(os.cpu_count() or 1)
+    import workloads as W
+    sample = args.ref_points
+    x, _, tau = W.random_points(sample, N_VARS, seed=7, tau_lo=TAU_LO)
+    dtau = np.full(sample, DTAU)
+    for _ in range(args.warmup):
+        o.pc_step(x, tau, dtau, K=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x, tau, st, dn = o.pc_step(x, tau, dtau, K=1)
+    dt = time.perf_counter() - t0
+    value = 2.0 * sample * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "BASELINE.json configs[2]: cyclic-10 Euler-Newton step (P:911-920), "
+                               f"bounded sample of {sample} points per step", "n": N_VARS,
+                   "terms": sysm.M, "lift_max": LIFT_MAX, "dtau": DTAU, "newton_iters": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{sample} cyclic-10 points x {args.steps} Euler-Newton steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(seconds_target=15.0):
+    """The oracle timed on a bounded sample of the same workload (rank 0, N = 1 only)."""
+    import oracle
+    import workloads as W
+    sysm = _system()
+    o = oracle.Oracle(sysm)
+    cores = oracle.set_threads(os.cpu_count() or 1)
+    probe = 1024
+    x, _, tau = W.random_points(probe, N_VARS, seed=7, tau_lo=TAU_LO)
+    t0 = time.perf_counter()
+    o.pc_step(x, tau, np.full(probe, DTAU), K=1)
+    dt = time.perf_counter() - t0
+    sample = int(min(1 << 17, max(probe, probe * seconds_target / max(dt, 1e-6))))
+    x, _, tau = W.random_points(sample, N_VARS, seed=7, tau_lo=TAU_LO)
+    t0 = time.perf_counter()
+    o.pc_step(x, tau, np.full(sample, DTAU), K=1)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * sample / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{sample} cyclic-10 points x 1 Euler-Newton step (2 evals + 2 solves each), "
+                      f"{dt:.1f} s on {cores} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--points", type=int, default=1 << 22, help="points per GPU")
+    ap.add_argument("--ref-points", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2111_14317_b200 as P
+    import workloads as W
+
+    sysm = _system()
+    g = P.System.from_workload(sysm, device=local)
+    Pn = args.points
+    # each rank its own shard of independent points (weak scaling; seeds differ per rank)
+    x_h, _, tau_h = W.random_points(Pn, N_VARS, seed=1000 + rank, tau_lo=TAU_LO)
+    x = torch.from_numpy(x_h).to(dev)
+    tau = torch.from_numpy(tau_h).to(dev)
+    dtau = torch.full((Pn,), DTAU, dtype=torch.float64, device=dev)
+    st = torch.empty(Pn, dtype=torch.uint8, device=dev)
+    dn = torch.empty(Pn, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        g.pc_step(x, tau, dtau, 1, st, dn)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches0 = P.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            g.pc_step(x, tau, dtau, 1, st, dn)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    launches = P.launch_count() - launches0
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    evals = 2.0 * Pn * world * args.steps
+    value = evals / (ms_max * 1e-3)
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    pin_x = torch.from_numpy(x_h).pin_memory()
+    pin_tau = torch.from_numpy(tau_h).pin_memory()
+    pin_dtau = torch.full((Pn,), DTAU, dtype=torch.float64).pin_memory()
+    xe, te, de = pin_x.numpy(), pin_tau.numpy(), pin_dtau.numpy()
+    g.pc_step_host(xe, te, de, 1)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        g.pc_step_host(xe, te, de, 1)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    te_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te_ms, op=dist.ReduceOp.MAX)
+    e2e_value = 2.0 * Pn * world * args.e2e_steps / (float(te_ms.item()) * 1e-3)
+
+    if rank == 0:
+        clocks = clk.summary() or {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        fl = algorithmic_flops_per_eval(sysm)
+        flops_launch = 2 * fl["total"] * Pn        # 2 evals + solves per point per pc_step launch
+        achieved = flops_launch / (ms_step * 1e-3) / 1e12
+        peak_mhz = clocks.get("sm_max_mhz") or 1965.0
+        peak = fp64_peak_tflops(peak_mhz)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "BASELINE.json configs[2]: cyclic-10 Euler-Newton step "
+                                   "(1 Euler prediction + 1 Newton iteration, P:911-920) on a batch of points",
+                       "points_per_gpu": Pn, "n": N_VARS, "terms": sysm.M, "lift_max": LIFT_MAX,
+                       "dtau": DTAU, "evals_per_point_step": 2, "parallelism": f"dp{world} (independent points)",
+                       "l2": "inputs larger than L2 (state %.0f MB > 126 MB)" % (Pn * (16 * N_VARS + 24) / 1e6)},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_pht<10,32,MODE_STEP>",
+                         "peak_basis": f"FP64 148 SM x 64 FMA/clk x 2 x {peak_mhz:.0f} MHz (DESIGN.md §5)",
+                         "flops_per_point_step": 2 * fl["total"]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pn * (16 * N_VARS + 16),
+                    "d2h_bytes_per_step": Pn * (16 * N_VARS + 8 + 1 + 8)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

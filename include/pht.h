@@ -1,0 +1,162 @@
+/*
+ * pht.h — C ABI of the B200-native polyhedral-homotopy hot path (arXiv 2111.14317).
+ *
+ * The library evaluates the polyhedral homotopy (Eq. (1))
+ *
+ *     h_k(x, t) = sum_{a in S_k} c_{k,a} x^a t^{omega_k(a)},    k = 1..n,
+ *
+ * together with dH/dx and dH/dt at large batches of points, in the logarithmic
+ * formulation of §5 (z = log x, monomials = exp(z_hat A_hat), derivatives =
+ * the same monomial row contracted against B_k, x-derivatives via diag(e^{-z})), and
+ * computes the consolidated Euler + Newton directions of §6 by solving
+ * Jx [dE | dN] = -[dH/dt | H] for both right-hand sides at once.  A fixed-protocol
+ * Euler-Newton step runs entirely on the device.
+ *
+ * Conventions (all functions):
+ *   - n = number of equations = number of variables (square systems).
+ *   - complex values are interleaved (re, im) double pairs — the memory layout of
+ *     torch.complex128 / numpy.complex128.  "c128[...]" below means 2*... doubles.
+ *   - Batched arrays are row-major, point-major: x[p][n], H[p][n], Jx[p][n][n] with Jx[q][k][j]
+ *     = dh_k/dx_j at point q (ledger R11 fixes the paper's vec() order).
+ *   - All point/output pointers are DEVICE pointers on the system's device, owned by the
+ *     caller; calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default
+ *     stream) and never synchronise the host (except the *_host variants).
+ *   - A NULL output pointer skips that output.
+ *   - API misuse returns a negative pht_status synchronously; numerical conditions are
+ *     reported per point in `status` (PHT_PT_* bits) and never abort the batch.
+ *   - The handle is immutable after creation and may be used from several streams.
+ */
+#ifndef PHT_H
+#define PHT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pht_system pht_system;
+
+typedef enum {
+    PHT_OK = 0,
+    PHT_EINVAL = -1,       /* bad argument (NULL, negative size, non-finite data)        */
+    PHT_ESHAPE = -2,       /* n_eq != n_var, n outside [1, PHT_MAX_N], bad offsets        */
+    PHT_EDUPLICATE = -3,   /* duplicate exponent vector inside one equation        */
+    PHT_EEMPTY = -4,       /* an equation has no term with a nonzero coefficient   */
+    PHT_ERANGE = -5,       /* |exponent| > PHT_MAX_EXP or lifting < 0                    */
+    PHT_ECUDA = -6,        /* a CUDA runtime call failed (see pht_last_cuda_error)        */
+    PHT_ENOMEM = -7,       /* device or host allocation failed                           */
+    PHT_EUNSUPPORTED = -8  /* option not supported by this build                         */
+} pht_status;
+
+/* per-point / per-path status bits */
+enum {
+    PHT_PT_OK = 0,
+    PHT_PT_ZERO_COORD = 1,     /* a coordinate is 0: outside (C*)^n          */
+    PHT_PT_NONFINITE = 2,      /* non-finite input or result                               */
+    PHT_PT_SINGULAR = 4,       /* |pivot| <= 1e-14 * (row max) in the direction solve       */
+    PHT_PT_STEP_UNDERFLOW = 8, /* tracker: step size fell below dtau_min                    */
+    PHT_PT_MAX_STEPS = 16,     /* tracker: step budget exhausted                            */
+    PHT_PT_DIVERGED = 32       /* tracker: endpoint not refined or ||x||_inf > inf_norm      */
+};
+
+#define PHT_MAX_N 24     /* largest n with a compiled kernel                              */
+#define PHT_MAX_EXP 1024 /* largest |exponent| accepted                                    */
+
+/*
+ * Load a system (Alg. 1 "Initialize").  All inputs are HOST pointers, copied.
+ *   n_eq, n_var   number of equations / variables; must be equal, 1..PHT_MAX_N.
+ *   eq_offsets    int64[n_eq+1], eq_offsets[0] = 0, non-decreasing; the terms of equation k
+ *                 are [eq_offsets[k], eq_offsets[k+1]) (per-equation supports S_k).
+ *   exponents     int32[M][n_var], M = eq_offsets[n_eq]; Laurent exponents a (may be < 0).
+ *   coeffs        c128[M] coefficients c_{k,a}.  Terms with c = 0 are dropped.
+ *   lifting       double[M] liftings omega_k(a) >= 0 (real values allowed on the GPU).
+ *   device        CUDA device ordinal that will own the tables and run every call.
+ *   out           receives the handle on success.
+ * Returns PHT_OK or a negative pht_status; *out is untouched on failure.
+ */
+int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *eq_offsets,
+                      const int32_t *exponents, const double *coeffs, const double *lifting,
+                      int32_t device, pht_system **out);
+
+/* Free the device tables.  NULL is a no-op.  No call may be in flight on the handle. */
+void pht_system_destroy(pht_system *sys);
+
+/* Query: n, number of packed terms M, largest equation size, owning device. */
+int pht_system_info(const pht_system *sys, int32_t *n, int64_t *M, int32_t *max_terms,
+                    int32_t *device);
+
+/*
+ * Batched evaluation of H, dH/dx, dH/dt (§5, Alg. 2).
+ *   p         number of points (>= 0; 0 is a no-op).
+ *   x         c128[p][n] points in (C*)^n.
+ *   t         double[p], t in (0, 1] (real homotopy parameter, ledger R2/R16; any t > 0 works).
+ *   H         c128[p][n]        h_k
+ *   Jx        c128[p][n][n]     dh_k/dx_j
+ *   Jt        c128[p][n]        dh_k/dt
+ *   row_exp2  int32[p][n] or NULL.  NULL: outputs are plain IEEE values (may overflow).
+ *             Non-NULL: every output of row k of point q is scaled by 2^-row_exp2[q][k]
+ *             (true row = returned row * 2^row_exp2, ledger R7); no overflow occurs.
+ *   status    uint8[p] PHT_PT_* bits, or NULL.
+ */
+int pht_evaluate(const pht_system *sys, int64_t p, const double *x, const double *t,
+                 double *H, double *Jx, double *Jt, int32_t *row_exp2, uint8_t *status,
+                 void *stream);
+
+/*
+ * The same in logarithmic coordinates: input z = log x (any branch;
+ * Im z is wrapped to (-pi, pi]) and tau = log t; outputs H, Jz = dH/dz = Jx diag(x),
+ * Jtau = dH/dtau = t dH/dt.  Range-safe with row_exp2 for |Re z| far beyond double range.
+ */
+int pht_evaluate_log(const pht_system *sys, int64_t p, const double *z, const double *tau,
+                     double *H, double *Jz, double *Jtau, int32_t *row_exp2, uint8_t *status,
+                     void *stream);
+
+/*
+ * Consolidated Euler + Newton directions (§6, affine form P:219-276):
+ *   Jx dE = -dH/dt   (dE = dx/dt, Davidenko)       Jx dN = -H   (Newton)
+ * computed from ONE elimination with two right-hand sides (partial pivoting).
+ *   x c128[p][n], t double[p] inputs; dE, dN c128[p][n] outputs; status as above
+ *   (PHT_PT_SINGULAR when a pivot is tiny; outputs of that point are then unspecified).
+ */
+int pht_euler_newton(const pht_system *sys, int64_t p, const double *x, const double *t,
+                     double *dE, double *dN, uint8_t *status, void *stream);
+
+/*
+ * The paper's simplified Euler-Newton step in tau = log t (Eq. (2)):
+ *   x~ = x + dtau * dx/dtau (Euler prediction),  tau~ = tau + dtau,
+ *   then newton_iters times:  x~ = x~ + dN(x~, tau~).
+ *   x         c128[p][n] in/out.
+ *   tau       double[p] in/out.
+ *   dtau      double[p] step sizes (tau + dtau should be <= 0).
+ *   newton_iters  K >= 0 Newton iterations (the paper's protocol uses 1).
+ *   status    uint8[p] or NULL (bits OR-ed over the step's solves).
+ *   dn_norm   double[p] or NULL: ||dN||_2 of the last Newton iteration.
+ */
+int pht_pc_step(const pht_system *sys, int64_t p, double *x, double *tau, const double *dtau,
+                int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream);
+
+/*
+ * pht_pc_step on HOST buffers (end-to-end entry point): copies x, tau, dtau to a device
+ * workspace owned by the handle, runs the step, copies x, tau, status, dn_norm back and
+ * synchronises.  Host pointers may be pageable or pinned.  Serialised per handle.
+ */
+int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
+                     const double *dtau, int32_t newton_iters, uint8_t *status,
+                     double *dn_norm, void *stream);
+
+/* Number of kernels this library has launched in the calling process (all handles). */
+int64_t pht_launch_count(void);
+
+/* Human-readable text for a pht_status; last CUDA error string for PHT_ECUDA. */
+const char *pht_strerror(int code);
+const char *pht_last_cuda_error(void);
+
+/* ABI version (incremented on any signature change). */
+int pht_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PHT_H */

@@ -1,0 +1,142 @@
+"""Thin Python surface over the C ABI (SURVEY §8(b) "Python surface").
+
+torch is used only for device memory and streams: every tensor handed to a call is a
+caller-owned CUDA buffer whose data_ptr() goes straight to the kernel; no arithmetic of the
+method happens here.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import PhtError, check  # noqa: F401
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class System:
+    """A loaded homotopy (pht_system_create).  Arguments as in include/pht.h."""
+
+    def __init__(self, offsets, exponents, coeffs, lifting, device: int = 0):
+        lib = _lib.load()
+        self._lib = lib
+        off = np.ascontiguousarray(offsets, np.int64)
+        exps = np.ascontiguousarray(exponents, np.int32)
+        c = np.ascontiguousarray(coeffs, np.complex128)
+        w = np.ascontiguousarray(lifting, np.float64)
+        n = int(exps.shape[1])
+        h = ctypes.c_void_p()
+        rc = lib.pht_system_create(len(off) - 1, n, off.ctypes.data_as(ctypes.c_void_p),
+                                   exps.ctypes.data_as(ctypes.c_void_p), c.ctypes.data_as(ctypes.c_void_p),
+                                   w.ctypes.data_as(ctypes.c_void_p), int(device), ctypes.byref(h))
+        check(rc, "pht_system_create")
+        self._h = h
+        self.device = int(device)
+        nn, M, mt, dev = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        check(lib.pht_system_info(h, ctypes.byref(nn), ctypes.byref(M), ctypes.byref(mt), ctypes.byref(dev)),
+              "pht_system_info")
+        self.n, self.M, self.max_terms = nn.value, M.value, mt.value
+
+    @classmethod
+    def from_workload(cls, system, device: int = 0):
+        return cls(system.offsets, system.exps, system.coeffs, system.lifting, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.pht_system_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    def _dev(self):
+        return torch.device("cuda", self.device)
+
+    def _check_pts(self, x, t):
+        if not (x.is_cuda and x.dtype == torch.complex128 and x.dim() == 2 and x.shape[1] == self.n
+                and x.is_contiguous()):
+            raise PhtError("x must be a contiguous cuda complex128 tensor [p, n]")
+        if not (t.is_cuda and t.dtype == torch.float64 and t.shape == (x.shape[0],) and t.is_contiguous()):
+            raise PhtError("t/tau must be a contiguous cuda float64 tensor [p]")
+
+    def evaluate(self, x, t, scaled: bool = False, out=None):
+        """H, Jx, Jt (+ row_exp2 if scaled), status at points x [p,n], t [p] (pht_evaluate)."""
+        self._check_pts(x, t)
+        p, n = x.shape
+        d = self._dev()
+        H = torch.empty((p, n), dtype=torch.complex128, device=d)
+        Jx = torch.empty((p, n, n), dtype=torch.complex128, device=d)
+        Jt = torch.empty((p, n), dtype=torch.complex128, device=d)
+        e2 = torch.empty((p, n), dtype=torch.int32, device=d) if scaled else None
+        st = torch.empty(p, dtype=torch.uint8, device=d)
+        check(self._lib.pht_evaluate(self._h, p, _ptr(x), _ptr(t), _ptr(H), _ptr(Jx), _ptr(Jt), _ptr(e2),
+                                     _ptr(st), _stream(d)), "pht_evaluate")
+        return (H, Jx, Jt, e2, st) if scaled else (H, Jx, Jt, st)
+
+    def evaluate_log(self, z, tau, scaled: bool = True):
+        """H, Jz = dH/dz, Jtau = dH/dtau (+ row_exp2) at z = log x, tau = log t."""
+        self._check_pts(z, tau)
+        p, n = z.shape
+        d = self._dev()
+        H = torch.empty((p, n), dtype=torch.complex128, device=d)
+        Jz = torch.empty((p, n, n), dtype=torch.complex128, device=d)
+        Jtau = torch.empty((p, n), dtype=torch.complex128, device=d)
+        e2 = torch.empty((p, n), dtype=torch.int32, device=d) if scaled else None
+        st = torch.empty(p, dtype=torch.uint8, device=d)
+        check(self._lib.pht_evaluate_log(self._h, p, _ptr(z), _ptr(tau), _ptr(H), _ptr(Jz), _ptr(Jtau),
+                                         _ptr(e2), _ptr(st), _stream(d)), "pht_evaluate_log")
+        return (H, Jz, Jtau, e2, st) if scaled else (H, Jz, Jtau, st)
+
+    def euler_newton(self, x, t):
+        """dE (Jx dE = -dH/dt), dN (Jx dN = -H), status (pht_euler_newton)."""
+        self._check_pts(x, t)
+        p, n = x.shape
+        d = self._dev()
+        dE = torch.empty((p, n), dtype=torch.complex128, device=d)
+        dN = torch.empty((p, n), dtype=torch.complex128, device=d)
+        st = torch.empty(p, dtype=torch.uint8, device=d)
+        check(self._lib.pht_euler_newton(self._h, p, _ptr(x), _ptr(t), _ptr(dE), _ptr(dN), _ptr(st),
+                                         _stream(d)), "pht_euler_newton")
+        return dE, dN, st
+
+    def pc_step(self, x, tau, dtau, newton_iters: int = 1, status=None, dn_norm=None):
+        """In-place Euler-Newton step (pht_pc_step); returns (status, dn_norm)."""
+        self._check_pts(x, tau)
+        p = x.shape[0]
+        d = self._dev()
+        if not (dtau.is_cuda and dtau.dtype == torch.float64 and dtau.shape == (p,)):
+            raise PhtError("dtau must be a cuda float64 tensor [p]")
+        st = status if status is not None else torch.empty(p, dtype=torch.uint8, device=d)
+        dn = dn_norm if dn_norm is not None else torch.empty(p, dtype=torch.float64, device=d)
+        check(self._lib.pht_pc_step(self._h, p, _ptr(x), _ptr(tau), _ptr(dtau), int(newton_iters), _ptr(st),
+                                    _ptr(dn), _stream(d)), "pht_pc_step")
+        return st, dn
+
+    def pc_step_host(self, x: np.ndarray, tau: np.ndarray, dtau: np.ndarray, newton_iters: int = 1):
+        """pht_pc_step_host on host numpy buffers (x, tau updated in place)."""
+        p = x.shape[0]
+        st = np.empty(p, np.uint8)
+        dn = np.empty(p, np.float64)
+        d = self._dev()
+        check(self._lib.pht_pc_step_host(self._h, p, x.ctypes.data_as(ctypes.c_void_p),
+                                         tau.ctypes.data_as(ctypes.c_void_p), dtau.ctypes.data_as(ctypes.c_void_p),
+                                         int(newton_iters), st.ctypes.data_as(ctypes.c_void_p),
+                                         dn.ctypes.data_as(ctypes.c_void_p), _stream(d)), "pht_pc_step_host")
+        return st, dn
+
+
+def launch_count() -> int:
+    return int(_lib.load().pht_launch_count())

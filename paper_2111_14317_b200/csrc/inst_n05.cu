@@ -1,0 +1,5 @@
+// Explicit instantiation of the k_pht launcher for n = 5 (one file per n: parallel build).
+#include "pht_kernels.cuh"
+namespace pht {
+template cudaError_t launch<5>(int, const DevSys &, const Args &, cudaStream_t);
+}

@@ -1,0 +1,5 @@
+// Explicit instantiation of the k_pht launcher for n = 6 (one file per n: parallel build).
+#include "pht_kernels.cuh"
+namespace pht {
+template cudaError_t launch<6>(int, const DevSys &, const Args &, cudaStream_t);
+}

@@ -1,0 +1,5 @@
+// Explicit instantiation of the k_pht launcher for n = 20 (one file per n: parallel build).
+#include "pht_kernels.cuh"
+namespace pht {
+template cudaError_t launch<20>(int, const DevSys &, const Args &, cudaStream_t);
+}

@@ -1,0 +1,310 @@
+// pht_capi.cu — C ABI (include/pht.h): system loader / packer (the
+// paper's Alg. 1 "Initialize") and the entry points that enqueue k_pht.
+#include "../../include/pht.h"
+#include "pht_kernels.cuh"
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+namespace pht {
+#define PHT_DECL(N) extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t);
+PHT_DECL(1) PHT_DECL(2) PHT_DECL(3) PHT_DECL(4) PHT_DECL(5) PHT_DECL(6) PHT_DECL(7) PHT_DECL(8)
+PHT_DECL(9) PHT_DECL(10) PHT_DECL(11) PHT_DECL(12) PHT_DECL(13) PHT_DECL(14) PHT_DECL(15)
+PHT_DECL(16) PHT_DECL(17) PHT_DECL(18) PHT_DECL(19) PHT_DECL(20) PHT_DECL(21) PHT_DECL(22)
+PHT_DECL(23) PHT_DECL(24)
+#undef PHT_DECL
+} // namespace pht
+
+static_assert(PHT_MAX_N == 24, "dispatch table below covers n = 1..24");
+
+struct pht_system {
+    int n = 0;
+    int64_t M = 0;
+    int max_terms = 0;
+    int device = 0;
+    double2 *d_rec = nullptr;
+    int *d_off = nullptr;
+    double *d_exptab = nullptr;
+    double2 *d_cistab = nullptr;
+    // workspace for the *_host entry points
+    std::mutex ws_mu;
+    int64_t ws_cap = 0;
+    void *ws = nullptr;
+};
+
+static thread_local std::string g_cuda_err;
+static std::atomic<int64_t> g_launches{0};
+
+static int cuda_fail(cudaError_t e)
+{
+    g_cuda_err = cudaGetErrorString(e);
+    return PHT_ECUDA;
+}
+
+struct DevGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DevGuard(int d)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != d) ok = cudaSetDevice(d) == cudaSuccess;
+    }
+    ~DevGuard()
+    {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
+                                 const double *coeffs, const double *lifting, int32_t device,
+                                 pht_system **out)
+{
+    if (!off || !exps || !coeffs || !lifting || !out) return PHT_EINVAL;
+    if (n_eq != n_var || n_eq < 1 || n_eq > PHT_MAX_N) return PHT_ESHAPE;
+    const int n = n_eq;
+    if (off[0] != 0) return PHT_ESHAPE;
+    for (int k = 0; k < n; ++k)
+        if (off[k + 1] < off[k]) return PHT_ESHAPE;
+    const int64_t M_in = off[n];
+    if (M_in >= (int64_t)1 << 30) return PHT_ESHAPE;
+
+    // a0: validate, drop zero coefficients, pack per-term records
+    //   [a_0 .. a_{n-1}, omega, log|c|, arg c, pad]   (DESIGN.md §2 "HBM/L1 layout")
+    const int RS = pht::rec_stride(n);
+    std::vector<double> rec;
+    std::vector<int> doff(n + 1, 0);
+    int max_terms = 0;
+    rec.reserve((size_t)M_in * RS);
+    int64_t M = 0;
+    for (int k = 0; k < n; ++k) {
+        std::set<std::vector<int32_t>> seen;
+        int cnt = 0;
+        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
+            std::vector<int32_t> a(exps + i * n, exps + (i + 1) * n);
+            if (!seen.insert(a).second) return PHT_EDUPLICATE;
+            for (int j = 0; j < n; ++j)
+                if (a[j] > PHT_MAX_EXP || a[j] < -PHT_MAX_EXP) return PHT_ERANGE;
+            const double cr = coeffs[2 * i], ci = coeffs[2 * i + 1], w = lifting[i];
+            if (!std::isfinite(cr) || !std::isfinite(ci) || !std::isfinite(w)) return PHT_EINVAL;
+            if (w < 0) return PHT_ERANGE;
+            if (cr == 0.0 && ci == 0.0) continue;
+            for (int j = 0; j < n; ++j) rec.push_back((double)a[j]);
+            rec.push_back(w);
+            rec.push_back(std::log(std::hypot(cr, ci)));
+            rec.push_back(std::atan2(ci, cr));
+            for (int u = n + 3; u < RS; ++u) rec.push_back(0.0);
+            ++cnt;
+            ++M;
+        }
+        if (cnt == 0) return PHT_EEMPTY;
+        doff[k + 1] = (int)M;
+        if (cnt > max_terms) max_terms = cnt;
+    }
+
+    // exp / cis tables, rounded from 80-bit long double
+    std::vector<double> etab(256), ctab(512);
+    const long double PI_L = 3.141592653589793238462643383279502884L;
+    for (int j = 0; j < 256; ++j) {
+        etab[j] = (double)exp2l((long double)j / 256.0L);
+        ctab[2 * j] = (double)cosl(2.0L * PI_L * (long double)j / 256.0L);
+        ctab[2 * j + 1] = (double)sinl(2.0L * PI_L * (long double)j / 256.0L);
+    }
+
+    DevGuard g(device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    pht_system *s = new (std::nothrow) pht_system();
+    if (!s) return PHT_ENOMEM;
+    s->n = n;
+    s->M = M;
+    s->max_terms = max_terms;
+    s->device = device;
+    cudaError_t e;
+    if ((e = cudaMalloc(&s->d_rec, rec.size() * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_off, doff.size() * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_exptab, 256 * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_cistab, 256 * sizeof(double2))) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_rec, rec.data(), rec.size() * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_off, doff.data(), doff.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_exptab, etab.data(), 256 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_cistab, ctab.data(), 512 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess) {
+        pht_system_destroy(s);
+        return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
+    }
+    *out = s;
+    return PHT_OK;
+}
+
+extern "C" void pht_system_destroy(pht_system *s)
+{
+    if (!s) return;
+    DevGuard g(s->device);
+    cudaFree(s->d_rec);
+    cudaFree(s->d_off);
+    cudaFree(s->d_exptab);
+    cudaFree(s->d_cistab);
+    cudaFree(s->ws);
+    delete s;
+}
+
+extern "C" int pht_system_info(const pht_system *s, int32_t *n, int64_t *M, int32_t *max_terms,
+                               int32_t *device)
+{
+    if (!s) return PHT_EINVAL;
+    if (n) *n = s->n;
+    if (M) *M = s->M;
+    if (max_terms) *max_terms = s->max_terms;
+    if (device) *device = s->device;
+    return PHT_OK;
+}
+
+static int dispatch(const pht_system *s, int mode, const pht::Args &A, void *stream)
+{
+    if (A.P == 0) return PHT_OK;
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    switch (s->n) {
+#define PHT_CASE(N) case N: e = pht::launch<N>(mode, S, A, st); break;
+        PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
+        PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12) PHT_CASE(13) PHT_CASE(14)
+        PHT_CASE(15) PHT_CASE(16) PHT_CASE(17) PHT_CASE(18) PHT_CASE(19) PHT_CASE(20) PHT_CASE(21)
+        PHT_CASE(22) PHT_CASE(23) PHT_CASE(24)
+#undef PHT_CASE
+    default: return PHT_ESHAPE;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return PHT_OK;
+}
+
+extern "C" int pht_evaluate(const pht_system *s, int64_t p, const double *x, const double *t, double *H,
+                            double *Jx, double *Jt, int32_t *row_exp2, uint8_t *status, void *stream)
+{
+    if (!s || p < 0 || (p > 0 && (!x || !t))) return PHT_EINVAL;
+    pht::Args A{};
+    A.P = p;
+    A.xin = (const double2 *)x;
+    A.tin = t;
+    A.H = (double2 *)H;
+    A.J = (double2 *)Jx;
+    A.Jt = (double2 *)Jt;
+    A.rexp = row_exp2;
+    A.status = status;
+    return dispatch(s, pht::MODE_EVAL_X, A, stream);
+}
+
+extern "C" int pht_evaluate_log(const pht_system *s, int64_t p, const double *z, const double *tau, double *H,
+                                double *Jz, double *Jtau, int32_t *row_exp2, uint8_t *status, void *stream)
+{
+    if (!s || p < 0 || (p > 0 && (!z || !tau))) return PHT_EINVAL;
+    pht::Args A{};
+    A.P = p;
+    A.xin = (const double2 *)z;
+    A.tin = tau;
+    A.H = (double2 *)H;
+    A.J = (double2 *)Jz;
+    A.Jt = (double2 *)Jtau;
+    A.rexp = row_exp2;
+    A.status = status;
+    return dispatch(s, pht::MODE_EVAL_Z, A, stream);
+}
+
+extern "C" int pht_euler_newton(const pht_system *s, int64_t p, const double *x, const double *t, double *dE,
+                                double *dN, uint8_t *status, void *stream)
+{
+    if (!s || p < 0 || (p > 0 && (!x || !t))) return PHT_EINVAL;
+    pht::Args A{};
+    A.P = p;
+    A.xin = (const double2 *)x;
+    A.tin = t;
+    A.dE = (double2 *)dE;
+    A.dN = (double2 *)dN;
+    A.status = status;
+    return dispatch(s, pht::MODE_DIRS, A, stream);
+}
+
+extern "C" int pht_pc_step(const pht_system *s, int64_t p, double *x, double *tau, const double *dtau,
+                           int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
+{
+    if (!s || p < 0 || newton_iters < 0 || (p > 0 && (!x || !tau || !dtau))) return PHT_EINVAL;
+    pht::Args A{};
+    A.P = p;
+    A.xio = (double2 *)x;
+    A.tauio = tau;
+    A.dtau = dtau;
+    A.K = newton_iters;
+    A.status = status;
+    A.dnnorm = dn_norm;
+    return dispatch(s, pht::MODE_STEP, A, stream);
+}
+
+extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, double *tau, const double *dtau,
+                                int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
+{
+    pht_system *s = const_cast<pht_system *>(cs);
+    if (!s || p < 0 || newton_iters < 0 || (p > 0 && (!x || !tau || !dtau))) return PHT_EINVAL;
+    if (p == 0) return PHT_OK;
+    std::lock_guard<std::mutex> lk(s->ws_mu);
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    const int n = s->n;
+    const size_t bx = (size_t)p * n * 16, bt = (size_t)p * 8, bs = (size_t)p;
+    const size_t need = bx + 3 * bt + bs + 64;
+    cudaError_t e;
+    if ((int64_t)need > s->ws_cap) {
+        cudaFree(s->ws);
+        s->ws = nullptr;
+        s->ws_cap = 0;
+        if ((e = cudaMalloc(&s->ws, need)) != cudaSuccess) return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
+        s->ws_cap = (int64_t)need;
+    }
+    char *w = (char *)s->ws;
+    double *dx = (double *)w, *dtu = (double *)(w + bx), *ddt = (double *)(w + bx + bt),
+           *ddn = (double *)(w + bx + 2 * bt);
+    uint8_t *dst = (uint8_t *)(w + bx + 3 * bt);
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((e = cudaMemcpyAsync(dx, x, bx, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dtu, tau, bt, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(ddt, dtau, bt, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_fail(e);
+    int rc = pht_pc_step(s, p, dx, dtu, ddt, newton_iters, dst, ddn, stream);
+    if (rc != PHT_OK) return rc;
+    if ((e = cudaMemcpyAsync(x, dx, bx, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(tau, dtu, bt, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (status && (e = cudaMemcpyAsync(status, dst, bs, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (dn_norm && (e = cudaMemcpyAsync(dn_norm, ddn, bt, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+        return cuda_fail(e);
+    return PHT_OK;
+}
+
+extern "C" int64_t pht_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char *pht_last_cuda_error(void) { return g_cuda_err.c_str(); }
+
+extern "C" const char *pht_strerror(int code)
+{
+    switch (code) {
+    case PHT_OK: return "ok";
+    case PHT_EINVAL: return "invalid argument";
+    case PHT_ESHAPE: return "shape error (square n in [1, PHT_MAX_N], monotone offsets)";
+    case PHT_EDUPLICATE: return "duplicate monomial in an equation";
+    case PHT_EEMPTY: return "equation without a nonzero term";
+    case PHT_ERANGE: return "exponent or lifting out of range";
+    case PHT_ECUDA: return "CUDA error";
+    case PHT_ENOMEM: return "out of memory";
+    case PHT_EUNSUPPORTED: return "unsupported";
+    default: return "unknown error";
+    }
+}
+
+extern "C" int pht_version(void) { return 1; }

@@ -1,0 +1,64 @@
+"""CPU-side checks of the boundary: libpht.so loads and exports every symbol include/pht.h
+declares; the Python binding declares a signature for each; no compute call is made."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "pht.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pht_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2111_14317_b200 import _lib
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = _header_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_binding_covers_header():
+    from paper_2111_14317_b200 import _lib
+    assert set(_header_functions()) == set(_lib.SIGNATURES)
+
+
+def test_version_and_strerror_without_gpu():
+    from paper_2111_14317_b200 import _lib
+    lib = _lib.load()
+    assert lib.pht_version() == 1
+    assert lib.pht_strerror(-3).decode().startswith("duplicate")
+    assert lib.pht_launch_count() >= 0
+
+
+def test_create_rejects_bad_shapes_before_touching_the_device():
+    """Validation errors are returned synchronously, before any CUDA call (so they work here)."""
+    import numpy as np
+    from paper_2111_14317_b200 import _lib
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    off = np.array([0, 2], np.int64)
+    ex = np.array([[1], [1]], np.int32)           # duplicate monomial
+    c = np.ones(2, np.complex128)
+    w = np.zeros(2)
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    assert lib.pht_system_create(1, 1, P(off), P(ex), P(c), P(w), 0, ctypes.byref(h)) == -3
+    assert lib.pht_system_create(1, 2, P(off), P(ex), P(c), P(w), 0, ctypes.byref(h)) == -2
+    ex2 = np.array([[1], [0]], np.int32)
+    assert lib.pht_system_create(1, 1, P(off), P(ex2), P(np.zeros(2, np.complex128)), P(w), 0,
+                                 ctypes.byref(h)) == -4
+    assert lib.pht_system_create(1, 1, P(off), P(ex2), P(c), P(-np.ones(2)), 0, ctypes.byref(h)) == -5
+
+
+def test_package_import_fails_loudly_without_library(tmp_path, monkeypatch):
+    from paper_2111_14317_b200 import _lib
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError):
+        _lib.load()
