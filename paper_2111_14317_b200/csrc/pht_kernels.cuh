@@ -1,13 +1,15 @@
 // pht_kernels.cuh — sm_100a kernels for the polyhedral-homotopy hot path (arXiv 2111.14317).
 //
-// One templated kernel, k_pht<N, PTS, MODE>, covers the four entry points of include/pht.h.
-// Mapping: a CTA owns a tile of PTS points; thread (k, q) = (equation k,
-// point q of the tile) computes ROW k of the extended Jacobian of point q
-//     [ dh_k/dz_1 .. dh_k/dz_N | dh_k/dtau | h_k ]        ("e^{z A} B_k^T")
-// in registers.  With PTS = 32 a warp holds one equation for 32 points, so every read of the
-// term table is a warp-uniform broadcast.  The rows of one point then stay in the registers
-// of N threads for the direction solve (Gauss-Jordan with partial pivoting, two right-hand
-// sides — §6 P:656-731 consolidated as in BASELINE.json north_star).
+// One templated kernel, k_pht<N, MODE>, covers the four entry points of include/pht.h.
+// Mapping: a CTA owns a tile of Geo<N>::PTS points and runs two layouts.
+//  * "W" (evaluation): thread (k, q) = (equation k, point q) computes ROW k of the extended
+//    Jacobian of point q, [ dh_k/dz_1 .. dh_k/dz_N | dh_k/dtau | h_k ] (P:525-542,
+//    "e^{z A} B_k^T"), in registers.  A warp holds one equation for 32 points, so every read of
+//    the term table is a warp-uniform broadcast.
+//  * "L" (direction solve): rows go through shared memory so that each warp owns whole points
+//    (lane = (point, row)); Gauss-Jordan with partial pivoting on [G | G_tau | h] for both
+//    right-hand sides (§6 P:656-731 consolidated as in BASELINE.json north_star) then needs
+//    only warp-level synchronisation (redux.sync argmax, __syncwarp pivot-row broadcast).
 //
 // Stages:
 //   a1  log split   rho = log|x_j|, vartheta = arg x_j, tau = log t
@@ -24,17 +26,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <cstddef>
+
 namespace pht {
 
 enum Mode : int { MODE_EVAL_X = 0, MODE_EVAL_Z = 1, MODE_DIRS = 2, MODE_STEP = 3 };
 
 enum : int { PT_ZERO_COORD = 1, PT_NONFINITE = 2, PT_SINGULAR = 4 };
 
-// Points per CTA tile for a given n (register budget: 65536 / (N * PTS) per thread).
-#ifndef PHT_PTS_SMALLN
-#define PHT_PTS_SMALLN 32
-#endif
-__host__ __device__ constexpr int pts_for(int n) { return n <= 12 ? PHT_PTS_SMALLN : 16; }
 // Term record stride in doubles: a_0..a_{n-1}, omega, log|c|, arg c, padded to even.
 __host__ __device__ constexpr int rec_stride(int n) { return (n + 3 + 1) & ~1; }
 
@@ -158,20 +158,50 @@ __device__ __forceinline__ double2 expcis(double y, double th, const double *eta
     return make_double2(mag * cr, mag * ci);
 }
 
-template <int N, int PTS>
+#ifndef PHT_RT_SMEM
+#define PHT_RT_SMEM(n) ((n) <= 12)
+#endif
+#ifndef PHT_PAIR
+#define PHT_PAIR(n) ((n) <= 8)
+#endif
+
+// ---- tile geometry --------------------------------------------------------------------
+// W layout (evaluation): WL point lanes per equation, thread (k, q) = (tid / WL, tid % WL).
+// L layout (solve): PPW points per warp, lane = (point, row).  PTS is chosen so that the L
+// groups exactly fill the CTA's warps (no second round), and CTAs stay small (<= 8 warps) so
+// that two co-resident CTAs overlap each other's load / barrier phases.
+template <int N>
+struct Geo {
+    static constexpr int WL = N <= 5 ? 32 : (N <= 16 ? 16 : 8);
+    static constexpr int NTW = N * WL;                 // W-layout threads
+    static constexpr int NWARP = (NTW + 31) / 32;
+    static constexpr int NT = NWARP * 32;              // threads per CTA (whole warps for the L layout)
+    static constexpr int PPW = 32 / N;                 // L layout: points per warp
+    static constexpr int GMAX = WL / PPW < NWARP ? WL / PPW : NWARP;
+    static constexpr int PTS = PPW * (GMAX > 0 ? GMAX : 1) <= WL ? PPW * (GMAX > 0 ? GMAX : 1) : WL;
+    static constexpr int NGRP = (PTS + PPW - 1) / PPW; // L-layout point groups (<= NWARP)
+    static constexpr int RW = N + 2;                   // row width (complex)
+    static constexpr int MS = (N * RW) | 1;            // matrix slot stride: odd => conflict-free
+    static constexpr int KS = (N + 3) & ~3;            // pivot-key slot per point (16 B aligned)
+    // co-resident CTAs per SM: aim at 16 warps (4 per SMSP -> 128 registers per thread)
+    static constexpr int MINB = N <= 12 ? (PHT_RT_SMEM(N) ? (16 / NWARP > 1 ? 16 / NWARP : 1) : 2) : 1;
+};
+
+template <int N>
 struct Smem {
+    static constexpr int WL = Geo<N>::WL;
     double exptab[256];
     double2 cistab[256];
-    double2 rt[N][PTS];   // (rho, vartheta) per variable; reused for dN staging in DIRS
-    double2 xs[N][PTS];   // x (or z) of the tile
-    double2 inv[N][PTS];  // 1/x (EVAL_X); reused for dE staging in DIRS
-    double tau[PTS];
-    double tinv[PTS];
-    int st[PTS];
-    double cand[N][PTS];  // pivot candidates
-    double2 prow[N + 2][PTS];
-    double2 pinv[PTS];
-    double dn2[N][PTS];
+    double2 rt[N][WL];    // (rho, vartheta) per variable
+    double2 xs[N][WL];    // x (or z) of the tile
+    double2 inv[N][WL];   // 1/x (EVAL_X); staging of dE (DIRS)
+    double2 out2[N][WL];  // staging of dN (DIRS)
+    double dn2[N][WL];
+    double tau[WL];
+    double tinv[WL];
+    int st[WL];
+    unsigned keys[Geo<N>::NWARP][Geo<N>::PPW * Geo<N>::KS]; // pivot keys (L layout)
+    double2 mat[Geo<N>::PTS * Geo<N>::MS]; // [q][row][col]: solve tile / staged evaluate output
 };
 
 // Term record -> registers: a_0..a_{N-1}, omega, log|c|, arg c (pht_capi.cu packer).
@@ -186,171 +216,177 @@ __device__ __forceinline__ void load_rec(const double2 *r, double (&a)[rec_strid
     }
 }
 
-// phi = omega tau + log|c| + sum_j a_j rho_j  with two interleaved partial sums (ILP).
+// (rho, vartheta) of one point: in registers, or read from the shared tile per term
+// (PHT_RT_SMEM: 4N fewer registers -> more resident warps; broadcast-free LDS.128 per variable).
+template <int N, bool SMEM>
+struct PointLog;
 template <int N>
-__device__ __forceinline__ double phi_of(const double (&a)[rec_stride(N)], const double (&rho)[N], double tau)
+struct PointLog<N, false> {
+    double rho[N], th[N];
+    template <int WL>
+    __device__ __forceinline__ void load(const double2 (*rt)[WL], int q)
+    {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double2 v = rt[j][q];
+            rho[j] = v.x;
+            th[j] = v.y;
+        }
+    }
+    __device__ __forceinline__ double2 get(int j) const { return make_double2(rho[j], th[j]); }
+};
+template <int N>
+struct PointLog<N, true> {
+    const double2 *base;
+    int stride;
+    template <int WL>
+    __device__ __forceinline__ void load(const double2 (*rt)[WL], int q)
+    {
+        base = &rt[0][q];
+        stride = WL;
+    }
+    __device__ __forceinline__ double2 get(int j) const { return base[j * stride]; }
+};
+
+// phi = omega tau + log|c| + sum_j a_j rho_j and theta = arg c + sum_j a_j vartheta_j, each with
+// two interleaved partial sums (ILP).
+template <int N, class PL>
+__device__ __forceinline__ void phi_theta(const double (&a)[rec_stride(N)], const PL &pl, double tau,
+                                          double &phi, double &theta)
+{
+    double p0 = fma(a[N], tau, a[N + 1]), p1 = 0.0, t0 = a[N + 2], t1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+        const double2 v = pl.get(j);
+        p0 = fma(a[j], v.x, p0);
+        t0 = fma(a[j], v.y, t0);
+        if (j + 1 < N) {
+            const double2 u = pl.get(j + 1);
+            p1 = fma(a[j + 1], u.x, p1);
+            t1 = fma(a[j + 1], u.y, t1);
+        }
+    }
+    phi = p0 + p1;
+    theta = t0 + t1;
+}
+
+template <int N, class PL>
+__device__ __forceinline__ double phi_of(const double (&a)[rec_stride(N)], const PL &pl, double tau)
 {
     double p0 = fma(a[N], tau, a[N + 1]), p1 = 0.0;
 #pragma unroll
     for (int j = 0; j < N; j += 2) {
-        p0 = fma(a[j], rho[j], p0);
-        if (j + 1 < N) p1 = fma(a[j + 1], rho[j + 1], p1);
+        p0 = fma(a[j], pl.get(j).x, p0);
+        if (j + 1 < N) p1 = fma(a[j + 1], pl.get(j + 1).x, p1);
     }
     return p0 + p1;
 }
 
+// Row accumulator with an online binary row exponent e (ledger R7): the row holds
+// sum_i w_i 2^-e; a term more than e^512 above the current scale rescales the row exactly.
 template <int N>
-__device__ __forceinline__ double theta_of(const double (&a)[rec_stride(N)], const double (&th)[N])
-{
-    double p0 = a[N + 2], p1 = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; j += 2) {
-        p0 = fma(a[j], th[j], p0);
-        if (j + 1 < N) p1 = fma(a[j + 1], th[j + 1], p1);
-    }
-    return p0 + p1;
-}
+struct RowAcc {
+    double2 g[N], gt, h;
+    double ed, eh, el;
 
-template <int N>
-__device__ __forceinline__ void accumulate(const double (&a)[rec_stride(N)], double2 w, double2 (&g)[N],
-                                           double2 &gt, double2 &h)
-{
-    h.x += w.x;
-    h.y += w.y;
-    gt.x = fma(a[N], w.x, gt.x);
-    gt.y = fma(a[N], w.y, gt.y);
+    __device__ __forceinline__ void init(double phi0)
+    {
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-        g[j].x = fma(a[j], w.x, g[j].x);
-        g[j].y = fma(a[j], w.y, g[j].y);
+        for (int j = 0; j < N; ++j) g[j] = make_double2(0.0, 0.0);
+        gt = h = make_double2(0.0, 0.0);
+        set_exp(rint(phi0 * INV_LN2));
     }
-}
+    __device__ __forceinline__ void set_exp(double e)
+    {
+        ed = e;
+        eh = e * LN2_HI;
+        el = e * LN2_LO;
+    }
+    __device__ __forceinline__ double reduce(double phi)
+    {
+        double y = (phi - eh) - el;
+        if (y > 512.0) { // rare: rescale everything to the new leading term (exact power of two)
+            const double e2 = rint(phi * INV_LN2);
+            const double f = scalbn(1.0, (int)fmax(ed - e2, -2000.0));
+#pragma unroll
+            for (int j = 0; j < N; ++j) g[j] = make_double2(g[j].x * f, g[j].y * f);
+            gt = make_double2(gt.x * f, gt.y * f);
+            h = make_double2(h.x * f, h.y * f);
+            set_exp(e2);
+            y = (phi - eh) - el;
+        }
+        return y;
+    }
+    __device__ __forceinline__ void add(const double (&a)[rec_stride(N)], double2 w)
+    {
+        h.x += w.x;
+        h.y += w.y;
+        gt.x = fma(a[N], w.x, gt.x);
+        gt.y = fma(a[N], w.y, gt.y);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            g[j].x = fma(a[j], w.x, g[j].x);
+            g[j].y = fma(a[j], w.y, g[j].y);
+        }
+    }
+};
 
 // a2-a4 for row k of point q: row = [G_1..G_N | G_tau | h] scaled by 2^-e.
 // Terms are processed two at a time (independent dependency chains for the FP64 pipe).
-template <int N, int PTS>
-__device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N, PTS> &sm, int k, int q,
+template <int N>
+__device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int k, int q,
                                          double2 (&row)[N + 2], int &e)
 {
     constexpr int RS = rec_stride(N);
-    double rho[N], th[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        const double2 v = sm.rt[j][q];
-        rho[j] = v.x;
-        th[j] = v.y;
-    }
+    PointLog<N, (bool)PHT_RT_SMEM(N)> pl;
+    pl.template load<Geo<N>::WL>(sm.rt, q);
     const double tau = sm.tau[q];
     const int i0 = __ldg(S.off + k), i1 = __ldg(S.off + k + 1);
     const double2 *rec = S.rec + (size_t)i0 * (RS / 2);
     const int m = i1 - i0;
 
-    // pass 1: row scale s = max_i (phi_i + log|c_i|)  (ledger R7)
-    double s0 = -INFINITY, s1 = -INFINITY;
+    RowAcc<N> acc;
+    {
+        double a[RS];
+        load_rec<N>(rec, a);
+        acc.init(phi_of<N>(a, pl, tau));
+    }
     int i = 0;
-    for (; i + 1 < m; i += 2) {
+    // two terms per iteration only while the register budget allows it (ILP vs spills)
+    for (; PHT_PAIR(N) && i + 1 < m; i += 2) {
         double a[RS], b[RS];
         load_rec<N>(rec + (size_t)i * (RS / 2), a);
         load_rec<N>(rec + (size_t)(i + 1) * (RS / 2), b);
-        s0 = fmax(s0, phi_of<N>(a, rho, tau));
-        s1 = fmax(s1, phi_of<N>(b, rho, tau));
-    }
-    if (i < m) {
-        double a[RS];
-        load_rec<N>(rec + (size_t)i * (RS / 2), a);
-        s0 = fmax(s0, phi_of<N>(a, rho, tau));
-    }
-    const double smax = fmax(s0, s1);
-    const double ed = isfinite(smax) ? rint(smax * INV_LN2) : 0.0;
-    e = (int)ed;
-    const double eh = ed * LN2_HI, el = ed * LN2_LO;
-
-    // pass 2: w_i = exp(phi_i - e ln2) cis(theta_i) and the contractions
-    double2 g[N], gt = make_double2(0.0, 0.0), h = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int j = 0; j < N; ++j) g[j] = make_double2(0.0, 0.0);
-    i = 0;
-    for (; i + 1 < m; i += 2) {
-        double a[RS], b[RS];
-        load_rec<N>(rec + (size_t)i * (RS / 2), a);
-        load_rec<N>(rec + (size_t)(i + 1) * (RS / 2), b);
-        const double ya = (phi_of<N>(a, rho, tau) - eh) - el;
-        const double yb = (phi_of<N>(b, rho, tau) - eh) - el;
-        const double ta = theta_of<N>(a, th), tb = theta_of<N>(b, th);
+        double pa, pb, ta, tb;
+        phi_theta<N>(a, pl, tau, pa, ta);
+        phi_theta<N>(b, pl, tau, pb, tb);
+        const double ya = acc.reduce(pa);
         const double2 wa = expcis(ya, ta, sm.exptab, sm.cistab);
+        const double yb = acc.reduce(pb);
         const double2 wb = expcis(yb, tb, sm.exptab, sm.cistab);
-        accumulate<N>(a, wa, g, gt, h);
-        accumulate<N>(b, wb, g, gt, h);
+        acc.add(a, wa);
+        acc.add(b, wb);
     }
-    if (i < m) {
+    for (; i < m; ++i) {
         double a[RS];
         load_rec<N>(rec + (size_t)i * (RS / 2), a);
-        const double ya = (phi_of<N>(a, rho, tau) - eh) - el;
-        const double2 wa = expcis(ya, theta_of<N>(a, th), sm.exptab, sm.cistab);
-        accumulate<N>(a, wa, g, gt, h);
+        double pa, ta;
+        phi_theta<N>(a, pl, tau, pa, ta);
+        const double ya = acc.reduce(pa);
+        acc.add(a, expcis(ya, ta, sm.exptab, sm.cistab));
     }
 #pragma unroll
-    for (int j = 0; j < N; ++j) row[j] = g[j];
-    row[N] = gt;
-    row[N + 1] = h;
-}
-
-// a5: Gauss-Jordan elimination with partial pivoting across the N row-threads of each point.
-// Pivot = max |Re|+|Im| of the column among rows not yet used, lowest row on ties (ledger R12).
-// On return the thread whose row was the pivot of column `col` holds
-//   dE = -row[N] / row[col],  dN = -row[N+1] / row[col]   (G [dE|dN] = -[G_tau | h]).
-template <int N, int PTS>
-__device__ __forceinline__ void gj_solve(Smem<N, PTS> &sm, int k, int q, double2 (&a)[N + 2],
-                                         int &col, double2 &dE, double2 &dN, bool &singular)
-{
-    double rmax = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j) rmax = fmax(rmax, cabs1(a[j]));
-    col = -1;
-    singular = false;
-    double2 myinv = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        double cand = -1.0;
-        if (col < 0) {
-            cand = cabs1(a[j]);
-            if (cand != cand) cand = INFINITY;
-        }
-        sm.cand[k][q] = cand;
-        __syncthreads();
-        int r = 0;
-        double best = sm.cand[0][q];
-#pragma unroll
-        for (int kk = 1; kk < N; ++kk) {
-            const double v = sm.cand[kk][q];
-            if (v > best) { best = v; r = kk; }
-        }
-        if (k == r) {
-            col = j;
-            const double pv = cabs1(a[j]);
-            if (!(pv > 1e-14 * rmax) || !isfinite(pv) || !isfinite(rmax)) singular = true;
-            myinv = crecip(a[j]);
-            sm.pinv[q] = myinv;
-#pragma unroll
-            for (int c = j + 1; c < N + 2; ++c) sm.prow[c][q] = a[c];
-        }
-        __syncthreads();
-        if (k != r) {
-            const double2 l = cmul(a[j], sm.pinv[q]);
-#pragma unroll
-            for (int c = j + 1; c < N + 2; ++c) a[c] = cfms(a[c], l, sm.prow[c][q]);
-            a[j] = make_double2(0.0, 0.0);
-        }
-    }
-    const double2 e = cmul(a[N], myinv), n = cmul(a[N + 1], myinv);
-    dE = make_double2(-e.x, -e.y);
-    dN = make_double2(-n.x, -n.y);
+    for (int j = 0; j < N; ++j) row[j] = acc.g[j];
+    row[N] = acc.gt;
+    row[N + 1] = acc.h;
+    e = (int)acc.ed;
 }
 
 // a1 for the whole tile: (rho, vartheta) from xs (x in EVAL_X/DIRS/STEP, z in EVAL_Z).
-template <int N, int PTS, int MODE>
-__device__ __forceinline__ void stage1(Smem<N, PTS> &sm, int tid)
+template <int N, int MODE>
+__device__ __forceinline__ void stage1(Smem<N> &sm, int tid)
 {
+    if (tid >= N * Geo<N>::PTS) return;
     const int q = tid / N, j = tid % N;
     const double2 v = sm.xs[j][q];
     double rho, th;
@@ -371,50 +407,157 @@ __device__ __forceinline__ void stage1(Smem<N, PTS> &sm, int tid)
     if (st) atomicOr(&sm.st[q], st);
 }
 
-template <int N, int PTS, int MODE>
-__global__ void __launch_bounds__(N *PTS, (N * PTS <= 192) ? 2 : 1) k_pht(const DevSys S, const Args A)
+// W -> shared: normalise the row by an exact power of two (rows are scale-free for the solve,
+// S:316) and store it into the point's matrix slot.
+template <int N>
+__device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&row)[N + 2])
 {
-    __shared__ Smem<N, PTS> sm;
+    double rmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) rmax = fmax(rmax, cabs1(row[j]));
+    if (rmax > 0.0 && isfinite(rmax)) {
+        const double f = scalbn(1.0, -ilogb(rmax));
+#pragma unroll
+        for (int c = 0; c < N + 2; ++c) row[c] = make_double2(row[c].x * f, row[c].y * f);
+    }
+    double2 *dst = sm.mat + q * Geo<N>::MS + k * Geo<N>::RW;
+#pragma unroll
+    for (int c = 0; c < N + 2; ++c) dst[c] = row[c];
+}
+
+// a5 in the L layout: lane (seg, i) of a warp holds row i of point q = g*PPW + seg.
+// Gauss-Jordan with partial pivoting (max |Re|+|Im| of the column among unused rows, lowest
+// row on ties — ledger R12; the comparison key keeps the top 15 mantissa bits).  The keys go
+// through shared memory (one STS, ceil(N/4) LDS.128, integer max); the pivot lane publishes its
+// row; elimination is branch-free (multiplier 0 on the pivot lane).  On return the lane whose row
+// pivoted column `col` holds dE = -row[N]/u, dN = -row[N+1]/u for variable col:
+// G [dE | dN] = -[G_tau | h].
+template <int N>
+__device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int &col, double2 &dE,
+                                       double2 &dN, bool &singular, bool &act, int &q)
+{
+    constexpr int RW = Geo<N>::RW, MS = Geo<N>::MS, PPW = Geo<N>::PPW, KS = Geo<N>::KS;
+    const int seg0 = lane / N;
+    const bool inseg = seg0 < PPW;
+    const int seg = inseg ? seg0 : 0, i = inseg ? lane - seg0 * N : 0;
+    q = g * PPW + seg;
+    act = inseg && (q < Geo<N>::PTS);
+    const int qc = (q < Geo<N>::PTS) ? q : 0;
+    double2 *slot = sm.mat + qc * MS;
+    unsigned *kseg = &sm.keys[w][seg * KS];
+    double2 a[RW];
+#pragma unroll
+    for (int c = 0; c < RW; ++c) a[c] = slot[i * RW + c];
+    double rmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) rmax = fmax(rmax, cabs1(a[j]));
+    __syncwarp();
+    bool used = false;
+    col = 0;
+    singular = !isfinite(rmax);
+    double2 myrcp = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        unsigned key = 0u;
+        if (!used) key = ((unsigned)__double2hiint(cabs1(a[j])) & ~63u) | (unsigned)(32 - i);
+        if (act) kseg[i] = key;
+        __syncwarp();
+        unsigned kmax = 0u;
+#pragma unroll
+        for (int u = 0; u < KS; u += 4) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(kseg + u);
+            kmax = max(kmax, (u + 0 < N) ? v.x : 0u);
+            kmax = max(kmax, (u + 1 < N) ? v.y : 0u);
+            kmax = max(kmax, (u + 2 < N) ? v.z : 0u);
+            kmax = max(kmax, (u + 3 < N) ? v.w : 0u);
+        }
+        const int r = 32 - (int)(kmax & 63u);
+        const bool me = (i == r);
+        if (me) {
+            used = true;
+            col = j;
+        }
+        if (me && act) {
+#pragma unroll
+            for (int c = j; c < RW; ++c) slot[r * RW + c] = a[c];
+        }
+        __syncwarp();
+        const double2 pv = slot[r * RW + j];
+        const double rd = __drcp_rn(fma(pv.x, pv.x, pv.y * pv.y));
+        const double2 rcp = make_double2(pv.x * rd, -pv.y * rd);
+        if (me) {
+            myrcp = rcp;
+            const double pa = cabs1(pv);
+            if (!(pa > 1e-14 * rmax) || !isfinite(pa) || !isfinite(rd)) singular = true;
+        }
+        // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row
+        double2 l = cmul(a[j], rcp);
+        l = me ? make_double2(0.0, 0.0) : l;
+#pragma unroll
+        for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, slot[r * RW + c]);
+        a[j] = me ? a[j] : make_double2(0.0, 0.0);
+        __syncwarp();
+    }
+    const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
+    dE = make_double2(-e.x, -e.y);
+    dN = make_double2(-n.x, -n.y);
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S, const Args A)
+{
+    using G = Geo<N>;
+    constexpr int PTS = G::PTS, WL = G::WL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
     const int tid = threadIdx.x;
-    const int k = tid / PTS, q = tid % PTS;
-    for (int i = tid; i < 256; i += N * PTS) {
+    const int k = tid / WL, q = tid % WL;           // W layout
+    const int lane = tid & 31, warp = tid >> 5;      // L layout
+    for (int i = tid; i < 256; i += G::NT) {
         sm.exptab[i] = __ldg(S.exptab + i);
         sm.cistab[i] = __ldg(S.cistab + i);
     }
     const int64_t base = (int64_t)blockIdx.x * PTS;
     const int64_t gq = base + q;
-    const bool valid = gq < A.P;
+    const bool valid = (k < N) && (q < PTS) && (gq < A.P);
 
     // load the tile's points, coalesced: flat element tid = (point tid/N, variable tid%N)
     const double2 *xsrc = (MODE == MODE_STEP) ? A.xio : A.xin;
-    {
+    if (tid < N * PTS) {
         const int qq = tid / N, j = tid % N;
         double2 v = make_double2(MODE == MODE_EVAL_Z ? 0.0 : 1.0, 0.0);
         if (base + qq < A.P) v = xsrc[(base * N) + tid];
         sm.xs[j][qq] = v;
     }
-    if (tid < PTS) {
+    if (tid < WL) {
         sm.st[tid] = 0;
         const int64_t g = base + tid;
+        const bool in = (tid < PTS) && (g < A.P);
         double tv = (MODE == MODE_EVAL_Z || MODE == MODE_STEP) ? 0.0 : 1.0;
-        if (g < A.P) tv = (MODE == MODE_STEP) ? A.tauio[g] : A.tin[g];
+        if (in) tv = (MODE == MODE_STEP) ? A.tauio[g] : A.tin[g];
         if (MODE == MODE_EVAL_Z || MODE == MODE_STEP) {
             sm.tau[tid] = tv;
-            if (!isfinite(tv)) sm.st[tid] |= PT_NONFINITE;
+            if (!isfinite(tv)) { sm.st[tid] |= PT_NONFINITE; sm.tau[tid] = 0.0; }
         } else {
             if (!(tv > 0.0) || !isfinite(tv)) { sm.st[tid] |= PT_NONFINITE; tv = 1.0; }
             sm.tau[tid] = log(tv);
             sm.tinv[tid] = 1.0 / tv;
         }
+        if (tid >= PTS) { // unused W lanes evaluate a harmless dummy point
+            for (int j = 0; j < N; ++j) sm.xs[j][tid] = make_double2(MODE == MODE_EVAL_Z ? 0.0 : 1.0, 0.0);
+        }
     }
     __syncthreads();
 
     if (MODE == MODE_EVAL_X || MODE == MODE_EVAL_Z) {
-        stage1<N, PTS, MODE>(sm, tid);
+        stage1<N, MODE>(sm, tid);
+        if (tid < WL && tid >= PTS)
+            for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
         __syncthreads();
         double2 row[N + 2];
-        int e;
-        eval_row<N, PTS>(S, sm, k, q, row, e);
+        int e = 0;
+        const bool wthr = k < N; // W-layout thread (the CTA is padded to whole warps)
+        if (wthr) eval_row<N>(S, sm, k, q, row, e);
         const bool scaled = A.rexp != nullptr;
         bool fin = true;
         if (MODE == MODE_EVAL_X) {
@@ -429,115 +572,146 @@ __global__ void __launch_bounds__(N *PTS, (N * PTS <= 192) ? 2 : 1) k_pht(const 
         }
 #pragma unroll
         for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(row[c].x) && isfinite(row[c].y);
-        if (!fin) atomicOr(&sm.st[q], PT_NONFINITE);
-        if (valid) {
-            const int64_t o = gq * N + k;
-            if (A.H) A.H[o] = row[N + 1];
-            if (A.Jt) A.Jt[o] = row[N];
-            if (A.J) {
-                double2 *dst = A.J + o * N;
+        if (wthr && !fin && q < PTS) atomicOr(&sm.st[q], PT_NONFINITE);
+        if (wthr && scaled && valid) A.rexp[gq * N + k] = e;
+        // stage the tile's rows in shared memory: [q][k][0..N-1 | Jt | H], then copy each output
+        // array's contiguous block with coalesced 16-byte stores
+        if (wthr && q < PTS) {
+            double2 *dst = sm.mat + q * Geo<N>::MS + k * Geo<N>::RW;
 #pragma unroll
-                for (int j = 0; j < N; ++j) dst[j] = row[j];
-            }
-            if (scaled) A.rexp[o] = e;
+            for (int c = 0; c < N + 2; ++c) dst[c] = row[c];
         }
         __syncthreads();
+        const int64_t npts = (A.P - base < PTS) ? (A.P - base) : PTS;
+        if (A.J) {
+            double2 *dstJ = A.J + base * N * N;
+            for (int u = tid; u < npts * N * N; u += G::NT) {
+                const int qq = u / (N * N), r = u - qq * N * N, kk = r / N, j = r - kk * N;
+                dstJ[u] = sm.mat[qq * Geo<N>::MS + kk * Geo<N>::RW + j];
+            }
+        }
+        for (int u = tid; u < npts * N; u += G::NT) {
+            const int qq = u / N, kk = u - qq * N;
+            const double2 *src = sm.mat + qq * Geo<N>::MS + kk * Geo<N>::RW;
+            if (A.Jt) A.Jt[base * N + u] = src[N];
+            if (A.H) A.H[base * N + u] = src[N + 1];
+        }
         if (tid < PTS && base + tid < A.P && A.status) A.status[base + tid] = (uint8_t)sm.st[tid];
         return;
     }
 
-    if (MODE == MODE_DIRS) {
-        stage1<N, PTS, MODE>(sm, tid);
-        __syncthreads();
-        double2 row[N + 2];
-        int e, col;
-        double2 dE, dN;
-        bool sing;
-        eval_row<N, PTS>(S, sm, k, q, row, e);
-        gj_solve<N, PTS>(sm, k, q, row, col, dE, dN, sing);
-        if (sing) atomicOr(&sm.st[q], PT_SINGULAR);
-        // dx/dt = x (.) delta_E / t,  dN_x = x (.) delta_N  (Jx = G diag(1/x), Jt = G_tau / t)
-        const double2 xv = sm.xs[col][q];
-        const double2 de = cmul(xv, dE), dn = cmul(xv, dN);
-        const double ti = sm.tinv[q];
-        sm.inv[col][q] = make_double2(de.x * ti, de.y * ti);
-        sm.rt[col][q] = dn;
+    // DIRS and STEP: evaluation (W) -> shared-memory tile -> warp-level solve (L).
+    const int iters = (MODE == MODE_STEP) ? A.K + 1 : 1;
+    for (int it = 0; it < iters; ++it) {
+        stage1<N, MODE>(sm, tid);
+        if (tid < WL && tid >= PTS)
+            for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
         __syncthreads();
         {
+            if (k < N) {
+                double2 row[N + 2];
+                int e;
+                eval_row<N>(S, sm, k, q, row, e);
+                if (q < PTS) store_row<N>(sm, k, q, row);
+            }
+        }
+        __syncthreads();
+        for (int g = warp; g < G::NGRP; g += G::NWARP) {
+            int col, qq;
+            double2 dE, dN;
+            bool sing, act;
+            lsolve<N>(sm, lane, warp, g, col, dE, dN, sing, act, qq);
+            if (act) {
+                if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
+                const double2 xv = sm.xs[col][qq];
+                if (MODE == MODE_DIRS) {
+                    // dx/dt = x (.) delta_E / t, dN_x = x (.) delta_N (Jx = G diag(1/x), Jt = G_tau/t)
+                    const double2 de = cmul(xv, dE), dn = cmul(xv, dN);
+                    const double ti = sm.tinv[qq];
+                    sm.inv[col][qq] = make_double2(de.x * ti, de.y * ti);
+                    sm.out2[col][qq] = dn;
+                } else if (it == 0) {
+                    // Euler: dx/dtau = x (.) delta_E  ->  x~ = x + h x delta_E
+                    const double h = (base + qq < A.P) ? A.dtau[base + qq] : 0.0;
+                    const double2 d = cmul(xv, dE);
+                    sm.xs[col][qq] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
+                } else {
+                    // Newton: x~ = x~ + x~ (.) delta_N
+                    const double2 d = cmul(xv, dN);
+                    sm.xs[col][qq] = make_double2(xv.x + d.x, xv.y + d.y);
+                    sm.dn2[col][qq] = fma(d.x, d.x, d.y * d.y);
+                }
+            }
+        }
+        __syncthreads();
+        if (MODE == MODE_STEP && it == 0 && tid < PTS)
+            sm.tau[tid] += (base + tid < A.P) ? A.dtau[base + tid] : 0.0;
+    }
+
+    if (MODE == MODE_DIRS) {
+        if (tid < N * PTS) {
             const int qq = tid / N, j = tid % N;
             if (base + qq < A.P) {
                 if (A.dE) A.dE[base * N + tid] = sm.inv[j][qq];
-                if (A.dN) A.dN[base * N + tid] = sm.rt[j][qq];
+                if (A.dN) A.dN[base * N + tid] = sm.out2[j][qq];
             }
         }
-        if (tid < PTS && base + tid < A.P && A.status) {
-            int st = sm.st[tid];
-            A.status[base + tid] = (uint8_t)st;
-        }
+        if (tid < PTS && base + tid < A.P && A.status) A.status[base + tid] = (uint8_t)sm.st[tid];
         return;
     }
-
-    // MODE_STEP: x~ = x + h dx/dtau ; tau~ = tau + h ; K x { x~ += dN(x~, tau~) }
-    {
-        double h = 0.0;
-        if (valid) h = A.dtau[gq];
-        for (int it = 0; it <= A.K; ++it) {
-            stage1<N, PTS, MODE>(sm, tid);
-            __syncthreads();
-            double2 row[N + 2];
-            int e, col;
-            double2 dE, dN;
-            bool sing;
-            eval_row<N, PTS>(S, sm, k, q, row, e);
-            gj_solve<N, PTS>(sm, k, q, row, col, dE, dN, sing);
-            if (sing) atomicOr(&sm.st[q], PT_SINGULAR);
-            const double2 xv = sm.xs[col][q];
-            if (it == 0) {
-                // dx/dtau = x (.) delta_E  ->  x~ = x + h x delta_E
-                const double2 d = cmul(xv, dE);
-                sm.xs[col][q] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
-            } else {
-                const double2 d = cmul(xv, dN);
-                sm.xs[col][q] = make_double2(xv.x + d.x, xv.y + d.y);
-                sm.dn2[col][q] = fma(d.x, d.x, d.y * d.y);
-            }
-            __syncthreads();
-            if (it == 0 && tid < PTS) sm.tau[tid] += (base + tid < A.P) ? A.dtau[base + tid] : 0.0;
-            // (the next iteration's stage1 is preceded by this barrier)
-            __syncthreads();
-        }
-        {
-            const int qq = tid / N;
-            if (base + qq < A.P) A.xio[base * N + tid] = sm.xs[tid % N][qq];
-        }
-        if (tid < PTS && base + tid < A.P) {
-            A.tauio[base + tid] = sm.tau[tid];
-            if (A.status) A.status[base + tid] = (uint8_t)sm.st[tid];
-            if (A.dnnorm) {
-                double s = 0.0;
-                for (int j = 0; j < N; ++j) s += sm.dn2[j][tid];
-                A.dnnorm[base + tid] = A.K > 0 ? sqrt(s) : 0.0;
-            }
+    // MODE_STEP epilogue
+    if (tid < N * PTS) {
+        const int qq = tid / N;
+        if (base + qq < A.P) A.xio[base * N + tid] = sm.xs[tid % N][qq];
+    }
+    if (tid < PTS && base + tid < A.P) {
+        A.tauio[base + tid] = sm.tau[tid];
+        if (A.status) A.status[base + tid] = (uint8_t)sm.st[tid];
+        if (A.dnnorm) {
+            double s2 = 0.0;
+            for (int j = 0; j < N; ++j) s2 += sm.dn2[j][tid];
+            A.dnnorm[base + tid] = A.K > 0 ? sqrt(s2) : 0.0;
         }
     }
+}
+
+template <int N, int MODE>
+size_t smem_bytes()
+{
+    return sizeof(Smem<N>);
+}
+
+template <int N, int MODE>
+cudaError_t launch_mode(const DevSys &S, const Args &A, cudaStream_t stream)
+{
+    constexpr int PTS = Geo<N>::PTS;
+    const int64_t tiles = (A.P + PTS - 1) / PTS;
+    if (tiles == 0) return cudaSuccess;
+    const size_t sb = smem_bytes<N, MODE>();
+    static std::atomic<unsigned long long> configured{0}; // one bit per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(k_pht<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        if (e != cudaSuccess) return e;
+        configured.fetch_or(bit);
+    }
+    k_pht<N, MODE><<<dim3((unsigned)tiles), dim3(Geo<N>::NT), sb, stream>>>(S, A);
+    return cudaGetLastError();
 }
 
 // Host-side launcher for one n (instantiated per n in inst_n*.cu).
 template <int N>
 cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream)
 {
-    constexpr int PTS = pts_for(N);
-    const int64_t tiles = (A.P + PTS - 1) / PTS;
-    if (tiles == 0) return cudaSuccess;
-    const dim3 grid((unsigned)tiles), block(N * PTS);
     switch (mode) {
-    case MODE_EVAL_X: k_pht<N, PTS, MODE_EVAL_X><<<grid, block, 0, stream>>>(S, A); break;
-    case MODE_EVAL_Z: k_pht<N, PTS, MODE_EVAL_Z><<<grid, block, 0, stream>>>(S, A); break;
-    case MODE_DIRS: k_pht<N, PTS, MODE_DIRS><<<grid, block, 0, stream>>>(S, A); break;
-    case MODE_STEP: k_pht<N, PTS, MODE_STEP><<<grid, block, 0, stream>>>(S, A); break;
+    case MODE_EVAL_X: return launch_mode<N, MODE_EVAL_X>(S, A, stream);
+    case MODE_EVAL_Z: return launch_mode<N, MODE_EVAL_Z>(S, A, stream);
+    case MODE_DIRS: return launch_mode<N, MODE_DIRS>(S, A, stream);
+    case MODE_STEP: return launch_mode<N, MODE_STEP>(S, A, stream);
     default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 } // namespace pht

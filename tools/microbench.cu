@@ -1,0 +1,157 @@
+// microbench.cu — B200 FP64 microbenchmarks used to set the roofline denominators and to guide
+// the kernel design.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+//   -o microbench tools/microbench.cu ; run on the GPU box.  Prints one JSON object.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e_)); return 1; } } while (0)
+
+// DFMA throughput: ILP independent chains per thread
+template <int ILP>
+__global__ void k_dfma(double *out, int iters, double a, double b)
+{
+    double x[ILP];
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < ILP; ++i) x[i] = fma(x[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) s += x[i];
+    if (s == 123.456) out[0] = s;
+}
+
+// dependent-chain latency: one warp, clock64 around a chain
+__global__ void k_dfma_lat(double *out, long long *cyc, int iters, double a, double b)
+{
+    double x = threadIdx.x * 1e-3;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        x = fma(x, a, b); x = fma(x, a, b); x = fma(x, a, b); x = fma(x, a, b);
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+    if (x == 123.456) out[0] = x;
+}
+
+__device__ __forceinline__ double2 libexpcis(double y, double th)
+{
+    double s, c;
+    sincos(th, &s, &c);
+    double m = exp(y);
+    return make_double2(m * c, m * s);
+}
+
+__global__ void k_libexpcis(double *out, int iters)
+{
+    double y = -threadIdx.x * 1e-3, th = threadIdx.x * 1e-2 + 0.3;
+    double2 acc = make_double2(0, 0);
+    for (int it = 0; it < iters; ++it) {
+        double2 w = libexpcis(y, th);
+        acc.x += w.x; acc.y += w.y;
+        y -= 1e-4; th += 0.37;
+    }
+    if (acc.x == 123.456) out[0] = acc.y;
+}
+
+__global__ void k_loglat(double *out, int iters)
+{
+    double x = 1.5 + threadIdx.x * 1e-3, y = 0.7, acc = 0;
+    for (int it = 0; it < iters; ++it) {
+        acc += 0.5 * log(fma(x, x, y * y)) + atan2(y, x);
+        x += 1e-4; y -= 1e-4;
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+int main()
+{
+    double *d;
+    long long *c;
+    CK(cudaMalloc(&d, 64));
+    CK(cudaMalloc(&c, 64));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int mhz = 0;
+    cudaDeviceGetAttribute(&mhz, cudaDevAttrClockRate, 0);
+    printf("{\"sms\": %d, \"clock_khz\": %d", sms, mhz);
+    // throughput: 148*8 blocks x 256 threads, ILP 8
+    {
+        const int iters = 20000, blocks = sms * 8, threads = 256;
+        k_dfma<8><<<blocks, threads>>>(d, 100, 1.0000001, 1e-9);
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0);
+        k_dfma<8><<<blocks, threads>>>(d, iters, 1.0000001, 1e-9);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * 8 * iters * (double)blocks * threads;
+        printf(", \"dfma_tflops\": %.3f", flops / (ms * 1e-3) / 1e12);
+    }
+    // throughput vs warps per SM with ILP 1 (latency hiding curve)
+    printf(", \"dfma_tflops_ilp1_by_warps_per_sm\": {");
+    for (int wps = 2; wps <= 32; wps *= 2) {
+        const int iters = 20000, blocks = sms, threads = 32 * wps;
+        k_dfma<1><<<blocks, threads>>>(d, 100, 1.0000001, 1e-9);
+        cudaEventRecord(e0);
+        k_dfma<1><<<blocks, threads>>>(d, iters, 1.0000001, 1e-9);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * iters * (double)blocks * threads;
+        printf("%s\"%d\": %.3f", wps == 2 ? "" : ", ", wps, flops / (ms * 1e-3) / 1e12);
+    }
+    printf("}");
+    printf(", \"dfma_tflops_ilp2_by_warps_per_sm\": {");
+    for (int wps = 2; wps <= 32; wps *= 2) {
+        const int iters = 20000, blocks = sms, threads = 32 * wps;
+        k_dfma<2><<<blocks, threads>>>(d, 100, 1.0000001, 1e-9);
+        cudaEventRecord(e0);
+        k_dfma<2><<<blocks, threads>>>(d, iters, 1.0000001, 1e-9);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double flops = 2.0 * 2 * iters * (double)blocks * threads;
+        printf("%s\"%d\": %.3f", wps == 2 ? "" : ", ", wps, flops / (ms * 1e-3) / 1e12);
+    }
+    printf("}");
+    {
+        k_dfma_lat<<<1, 32>>>(d, c, 1000, 1.0000001, 1e-9);
+        CK(cudaDeviceSynchronize());
+        long long cy;
+        cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
+        printf(", \"dfma_latency_cycles\": %.2f", cy / 4000.0);
+    }
+    {
+        const int iters = 2000, blocks = sms * 4, threads = 256;
+        k_libexpcis<<<blocks, threads>>>(d, 10);
+        cudaEventRecord(e0);
+        k_libexpcis<<<blocks, threads>>>(d, iters);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf(", \"libdevice_exp_sincos_G_per_s\": %.3f", iters * (double)blocks * threads / (ms * 1e-3) / 1e9);
+    }
+    {
+        const int iters = 2000, blocks = sms * 4, threads = 256;
+        k_loglat<<<blocks, threads>>>(d, 10);
+        cudaEventRecord(e0);
+        k_loglat<<<blocks, threads>>>(d, iters);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf(", \"libdevice_log_atan2_G_per_s\": %.3f", iters * (double)blocks * threads / (ms * 1e-3) / 1e9);
+    }
+    printf("}\n");
+    return 0;
+}
