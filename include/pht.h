@@ -145,6 +145,43 @@ int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
                      const double *dtau, int32_t newton_iters, uint8_t *status,
                      double *dn_norm, void *stream);
 
+/*
+ * Adaptive path tracking tau0 -> 0 on the device (step control = DESIGN.md
+ * reading R14, the same algorithm as the oracle's tracker).  One persistent kernel: each slot
+ * of each CTA runs one path (Euler predictor from dx/dtau, up to newton_iters Newton
+ * corrections, accept -> grow dtau by `grow` after `grow_after` successes, reject -> shrink),
+ * lands exactly on tau = 0, then refines with up to final_iters Newton steps at t = 1;
+ * finished slots take the next path from an atomic queue.
+ *   x       c128[p][n] start points in (on their paths at tau), endpoints out.
+ *   tau     double[p] start parameters tau0 <= 0 in; final tau (0 when tracked) out.
+ *   opts    options; NULL = defaults (pht_track_opts_default).
+ *   stats   int64[p][4] or NULL: accepted steps, rejected steps, evaluations (each one
+ *           evaluate + 2-RHS solve), final Newton iterations.
+ *   status  uint8[p]: PHT_PT_OK = finite converged endpoint; PHT_PT_SINGULAR,
+ *           PHT_PT_STEP_UNDERFLOW, PHT_PT_MAX_STEPS, PHT_PT_DIVERGED (refinement failed or
+ *           ||x||_inf > inf_norm), PHT_PT_NONFINITE (non-finite tau0).
+ * Asynchronous on `stream`; uses a stream-ordered 8-byte device counter.
+ */
+typedef struct {
+    double dtau_init;   /* 0.05   initial step in tau                                   */
+    double dtau_min;    /* 1e-8   step underflow threshold                              */
+    double dtau_max;    /* 0.5                                                           */
+    double newton_tol;  /* 1e-10  corrector: max_j |dN_j|/|x_j| <= newton_tol             */
+    double shrink;      /* 0.5                                                           */
+    double grow;        /* 2.0                                                           */
+    double final_tol;   /* 1e-13  final refinement: max_j |dN_j|/|x_j| <= final_tol       */
+    double inf_norm;    /* 1e8    endpoints with ||x||_inf above this are DIVERGED         */
+    int32_t newton_iters; /* 4    max corrector iterations per step (K)                  */
+    int32_t grow_after;   /* 3                                                           */
+    int32_t max_steps;    /* 10000                                                       */
+    int32_t final_iters;  /* 5                                                           */
+} pht_track_opts;
+
+void pht_track_opts_default(pht_track_opts *opts);
+
+int pht_track(const pht_system *sys, int64_t p, double *x, double *tau, const pht_track_opts *opts,
+              int64_t *stats, uint8_t *status, void *stream);
+
 /* Number of kernels this library has launched in the calling process (all handles). */
 int64_t pht_launch_count(void);
 

@@ -454,7 +454,13 @@ int orc_dirs_qr(int n, const double *J, double *dE, double *dN)
 /* ------------------------------------------------------------------ */
 /* directions and steps                        */
 /* ------------------------------------------------------------------ */
-/* Solve at one point: dE = dx/dt with Jx dE = -dH/dt, dN with Jx dN = -H. */
+/*
+ * Solve at one point: dE = dx/dt with Jx dE = -dH/dt, dN with Jx dN = -H.
+ * The system is solved in logarithmic coordinates: Jz = Jx diag(x) = dH/dz (the
+ * chain rule of the diag(e^{-z}) rescale), Jz delta = -rhs, dx = x (.) delta.  This is
+ * the same solution; it keeps the row-relative singular test (reading R13) independent of the
+ * scale of the coordinates, which for polyhedral start points spans many orders of magnitude.
+ */
 static int solve_point(const orc_sys *s, const double *xp, double t, double *dE, double *dN)
 {
     const int n = s->n;
@@ -462,6 +468,8 @@ static int solve_point(const orc_sys *s, const double *xp, double t, double *dE,
     int st = eval_point(s, xp, t, H, Jx, Jt, 0, 0, 0);
     if (st) return st;
     for (int k = 0; k < n; ++k) {
+        for (int j = 0; j < n; ++j) /* Jz[k][j] = Jx[k][j] * x_j */
+            store(Jx + 2 * (k * n + j), cmul(load(Jx + 2 * (k * n + j)), load(xp + 2 * j)));
         B[2 * (k * 2 + 0) + 0] = -Jt[2 * k];
         B[2 * (k * 2 + 0) + 1] = -Jt[2 * k + 1];
         B[2 * (k * 2 + 1) + 0] = -H[2 * k];
@@ -470,8 +478,9 @@ static int solve_point(const orc_sys *s, const double *xp, double t, double *dE,
     st = orc_lu_solve(n, 2, Jx, B, X);
     if (st) return st;
     for (int k = 0; k < n; ++k) {
-        if (dE) { dE[2 * k] = X[2 * (k * 2)]; dE[2 * k + 1] = X[2 * (k * 2) + 1]; }
-        if (dN) { dN[2 * k] = X[2 * (k * 2 + 1)]; dN[2 * k + 1] = X[2 * (k * 2 + 1) + 1]; }
+        const cplx xk = load(xp + 2 * k);
+        if (dE) store(dE + 2 * k, cmul(xk, load(X + 2 * (k * 2))));
+        if (dN) store(dN + 2 * k, cmul(xk, load(X + 2 * (k * 2 + 1))));
     }
     for (int k = 0; k < 2 * n; ++k)
         if ((dE && !isfinite(dE[k])) || (dN && !isfinite(dN[k]))) return ORC_PT_NONFINITE;
@@ -531,8 +540,23 @@ int orc_pc_step(int n, const int64_t *off, const int32_t *a, const double *c, co
     return 0;
 }
 
+/* max_j |d_j| / |x_j|: componentwise relative size of a correction (reading R14). */
+static double relmax(int n, const double *d, const double *x)
+{
+    double r = 0.0;
+    for (int j = 0; j < n; ++j) {
+        double ax = hypot(x[2 * j], x[2 * j + 1]);
+        double ad = hypot(d[2 * j], d[2 * j + 1]);
+        double q = ad / ax;
+        if (!(q <= r)) r = q; /* NaN propagates */
+    }
+    return r;
+}
+
 /*
- * Adaptive tracking tau0 -> 0 (step control = DESIGN.md reading R14).
+ * Adaptive tracking tau0 -> 0 (step control = DESIGN.md reading R14: the
+ * corrector converges when max_j |dN_j|/|x_j| <= newton_tol, a scale-invariant test because
+ * polyhedral start points span many orders of magnitude).
  * opt[] = {dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm}
  * iopt[] = {K (max corrector iters), grow_after, max_steps, final_iters}
  * stats[q] = {accepted steps, rejected steps, evaluations (solves), final Newton iters}.
@@ -552,6 +576,11 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
         int succ = 0, st = 0;
+        if (!isfinite(tq)) {
+            status[q] = ORC_PT_NONFINITE;
+            for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
+            continue;
+        }
         while (tq < 0.0) {
             if (steps == max_steps) { st = ORC_PT_MAX_STEPS; break; }
             double h = fmin(dt, -tq);
@@ -566,9 +595,9 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
                     s1 = solve_point(&s, xt, exp(tt), 0, dN);
                     ++evals;
                     if (s1) break;
+                    double nd = relmax(n, dN, xt);
                     for (int i = 0; i < 2 * n; ++i) xt[i] += dN[i];
-                    double nd = vnorm(n, dN);
-                    if (nd <= newton_tol * vnorm(n, xt)) { ok = 1; break; }
+                    if (nd <= newton_tol) { ok = 1; break; }
                     if (it >= 2 && nd > 0.5 * prev) break;
                     prev = nd;
                 }
@@ -591,8 +620,9 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
                 int s1 = solve_point(&s, xq, 1.0, 0, dN);
                 ++evals; ++fin;
                 if (s1) break;
+                double nd = relmax(n, dN, xq);
                 for (int i = 0; i < 2 * n; ++i) xq[i] += dN[i];
-                if (vnorm(n, dN) <= final_tol * vnorm(n, xq)) { conv = 1; break; }
+                if (nd <= final_tol) { conv = 1; break; }
             }
             double xinf = 0.0;
             for (int j = 0; j < n; ++j) xinf = fmax(xinf, cabs(load(xq + 2 * j)));

@@ -31,11 +31,21 @@ SIGNATURES = {
     "pht_euler_newton": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_pc_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "pht_pc_step_host": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "pht_track_opts_default": (None, [ctypes.c_void_p]),
+    "pht_track": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_launch_count": (_i64, []),
     "pht_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "pht_last_cuda_error": (ctypes.c_char_p, []),
     "pht_version": (ctypes.c_int, []),
 }
+
+
+class TrackOpts(ctypes.Structure):
+    """pht_track_opts (include/pht.h)."""
+    _fields_ = [("dtau_init", ctypes.c_double), ("dtau_min", ctypes.c_double), ("dtau_max", ctypes.c_double),
+                ("newton_tol", ctypes.c_double), ("shrink", ctypes.c_double), ("grow", ctypes.c_double),
+                ("final_tol", ctypes.c_double), ("inf_norm", ctypes.c_double), ("newton_iters", ctypes.c_int32),
+                ("grow_after", ctypes.c_int32), ("max_steps", ctypes.c_int32), ("final_iters", ctypes.c_int32)]
 
 
 class PhtError(RuntimeError):

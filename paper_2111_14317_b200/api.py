@@ -137,6 +137,25 @@ class System:
                                          dn.ctypes.data_as(ctypes.c_void_p), _stream(d)), "pht_pc_step_host")
         return st, dn
 
+    def track(self, x, tau, stats: bool = True, **opts):
+        """Adaptive tracking tau0 -> 0 in place (pht_track).  x: complex128 [p, n] start points,
+        tau: float64 [p] start parameters.  Keyword options = pht_track_opts fields.
+        Returns (status uint8 [p], stats int64 [p, 4] or None)."""
+        self._check_pts(x, tau)
+        p = x.shape[0]
+        d = self._dev()
+        o = _lib.TrackOpts()
+        self._lib.pht_track_opts_default(ctypes.byref(o))
+        for k, v in opts.items():
+            if not hasattr(o, k):
+                raise PhtError(f"unknown tracker option {k}")
+            setattr(o, k, v)
+        st = torch.empty(p, dtype=torch.uint8, device=d)
+        sv = torch.empty((p, 4), dtype=torch.int64, device=d) if stats else None
+        check(self._lib.pht_track(self._h, p, _ptr(x), _ptr(tau), ctypes.byref(o), _ptr(sv), _ptr(st),
+                                  _stream(d)), "pht_track")
+        return st, sv
+
 
 def launch_count() -> int:
     return int(_lib.load().pht_launch_count())

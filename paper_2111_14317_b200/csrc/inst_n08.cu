@@ -1,5 +1,6 @@
-// Explicit instantiation of the k_pht launcher for n = 8 (one file per n: parallel build).
+// Explicit instantiation of the launchers for n = 8 (one file per n: parallel build).
 #include "pht_kernels.cuh"
 namespace pht {
 template cudaError_t launch<8>(int, const DevSys &, const Args &, cudaStream_t);
+template cudaError_t launch_track<8>(const DevSys &, const TrackArgs &, cudaStream_t, int);
 }

@@ -13,7 +13,9 @@
 #include <vector>
 
 namespace pht {
-#define PHT_DECL(N) extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t);
+#define PHT_DECL(N)                                                                             \
+    extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t);     \
+    extern template cudaError_t launch_track<N>(const DevSys &, const TrackArgs &, cudaStream_t, int);
 PHT_DECL(1) PHT_DECL(2) PHT_DECL(3) PHT_DECL(4) PHT_DECL(5) PHT_DECL(6) PHT_DECL(7) PHT_DECL(8)
 PHT_DECL(9) PHT_DECL(10) PHT_DECL(11) PHT_DECL(12) PHT_DECL(13) PHT_DECL(14) PHT_DECL(15)
 PHT_DECL(16) PHT_DECL(17) PHT_DECL(18) PHT_DECL(19) PHT_DECL(20) PHT_DECL(21) PHT_DECL(22)
@@ -28,6 +30,7 @@ struct pht_system {
     int64_t M = 0;
     int max_terms = 0;
     int device = 0;
+    int sms = 148;
     double2 *d_rec = nullptr;
     int *d_off = nullptr;
     double *d_exptab = nullptr;
@@ -125,6 +128,7 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     s->M = M;
     s->max_terms = max_terms;
     s->device = device;
+    cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e;
     if ((e = cudaMalloc(&s->d_rec, rec.size() * sizeof(double))) != cudaSuccess ||
         (e = cudaMalloc(&s->d_off, doff.size() * sizeof(int))) != cudaSuccess ||
@@ -284,6 +288,67 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
         (dn_norm && (e = cudaMemcpyAsync(dn_norm, ddn, bt, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
         (e = cudaStreamSynchronize(st)) != cudaSuccess)
         return cuda_fail(e);
+    return PHT_OK;
+}
+
+extern "C" void pht_track_opts_default(pht_track_opts *o)
+{
+    if (!o) return;
+    o->dtau_init = 0.05;
+    o->dtau_min = 1e-8;
+    o->dtau_max = 0.5;
+    o->newton_tol = 1e-10;
+    o->shrink = 0.5;
+    o->grow = 2.0;
+    o->final_tol = 1e-13;
+    o->inf_norm = 1e8;
+    o->newton_iters = 4;
+    o->grow_after = 3;
+    o->max_steps = 10000;
+    o->final_iters = 5;
+}
+
+extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau, const pht_track_opts *opts,
+                         int64_t *stats, uint8_t *status, void *stream)
+{
+    if (!s || p < 0 || (p > 0 && (!x || !tau || !status))) return PHT_EINVAL;
+    if (p == 0) return PHT_OK;
+    pht_track_opts o;
+    if (opts) o = *opts;
+    else pht_track_opts_default(&o);
+    if (!(o.dtau_init > 0) || !(o.dtau_min > 0) || !(o.dtau_max > 0) || !(o.shrink > 0 && o.shrink < 1) ||
+        !(o.grow >= 1) || o.newton_iters < 1 || o.grow_after < 1 || o.max_steps < 1 || o.final_iters < 0)
+        return PHT_EINVAL;
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *ctr = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
+    pht::TrackArgs A{};
+    A.P = p;
+    A.x = (double2 *)x;
+    A.tau = tau;
+    A.status = status;
+    A.stats = (long long *)stats;
+    A.queue = ctr;
+    A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
+                         o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters};
+    switch (s->n) {
+#define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms); break;
+        PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
+        PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12) PHT_CASE(13) PHT_CASE(14)
+        PHT_CASE(15) PHT_CASE(16) PHT_CASE(17) PHT_CASE(18) PHT_CASE(19) PHT_CASE(20) PHT_CASE(21)
+        PHT_CASE(22) PHT_CASE(23) PHT_CASE(24)
+#undef PHT_CASE
+    default: e = cudaErrorInvalidValue;
+    }
+    cudaError_t e2 = cudaFreeAsync(ctr, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (e2 != cudaSuccess) return cuda_fail(e2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     return PHT_OK;
 }
 

@@ -61,6 +61,21 @@ struct Args {
     int K;               // STEP: Newton iterations
 };
 
+// Tracker options (include/pht.h pht_track_opts) and arguments.
+struct TrackOpts {
+    double dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm;
+    int K, grow_after, max_steps, final_iters;
+};
+struct TrackArgs {
+    int64_t P;
+    double2 *x;          // [P][N] start points in, endpoints out
+    double *tau;         // [P] tau0 in, final tau out
+    uint8_t *status;     // [P]
+    long long *stats;    // [P][4] accepted steps, rejected steps, evaluations, final iterations
+    unsigned long long *queue; // path counter (zeroed by the host)
+    TrackOpts o;
+};
+
 // ---- constants (Cody-Waite splits computed with 80-digit arithmetic) ----
 __device__ constexpr double SHIFT = 0x1.8p52;               // round-to-integer shifter
 __device__ constexpr double INV_LN2 = 0x1.71547652b82fep+0;
@@ -673,6 +688,267 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
             A.dnnorm[base + tid] = A.K > 0 ? sqrt(s2) : 0.0;
         }
     }
+}
+
+
+// ---------------------------------------------------------------------------------------
+// a6: persistent device tracker (SURVEY §8(a) a6, step control = DESIGN.md reading R14).
+// Every CTA slot runs one path as a state machine; every loop iteration performs one
+// evaluation + two-RHS solve for all slots at their current query point:
+//   PREDICT  query (x, tau):    x~ = x + h dx/dtau, tau~ = tau + h, h = min(dtau, -tau)
+//   CORRECT  query (x~, tau~):  x~ += dN; converged -> accept, contraction/K exhausted -> reject
+//   FINAL    query (x, 0):      x += dN until ||dN|| <= final_tol ||x|| (<= final_iters)
+// Finished slots write their path back and take the next index from a global atomic queue.
+enum : int { PH_IDLE = 0, PH_PREDICT = 1, PH_CORRECT = 2, PH_FINAL = 3 };
+
+template <int N>
+struct TrackSmem {
+    Smem<N> s;
+    double2 xa[N][Geo<N>::WL];   // accepted point
+    double2 xt[N][Geo<N>::WL];   // trial point
+    double2 dd[N][Geo<N>::WL];   // direction of this iteration (delta_E or delta_N, log coords)
+    double nd2[N][Geo<N>::WL];   // |dx_j|^2 of this iteration
+    double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL];
+    long long path[Geo<N>::WL], steps[Geo<N>::WL], rej[Geo<N>::WL], evals[Geo<N>::WL], fin[Geo<N>::WL];
+    int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL];
+    int acc[Geo<N>::WL];         // this iteration: 1 accept x~ -> x
+    long long done_path[Geo<N>::WL]; // path finished this iteration (-1 none)
+    int refill[Geo<N>::WL];      // 1: load a new path into the slot
+    int active;
+};
+
+template <int N>
+__device__ __forceinline__ void trk_pop(TrackSmem<N> &T, const TrackArgs &A, int q)
+{
+    unsigned long long idx = atomicAdd(A.queue, 1ull);
+    while ((long long)idx < A.P && !isfinite(A.tau[idx])) { // unusable start: report and skip
+        A.status[idx] = (uint8_t)PT_NONFINITE;
+        if (A.stats)
+            for (int u = 0; u < 4; ++u) A.stats[4 * idx + u] = 0;
+        idx = atomicAdd(A.queue, 1ull);
+    }
+    if ((long long)idx < A.P) {
+        T.path[q] = (long long)idx;
+        T.refill[q] = 1;
+        const double t0 = A.tau[idx];
+        T.tau_a[q] = t0;
+        T.dt[q] = A.o.dtau_init;
+        T.steps[q] = T.rej[q] = T.evals[q] = T.fin[q] = 0;
+        T.succ[q] = 0;
+        T.it[q] = 0;
+        T.phase[q] = (t0 < 0.0) ? PH_PREDICT : PH_FINAL;
+    } else {
+        T.path[q] = -1;
+        T.refill[q] = 0;
+        T.phase[q] = PH_IDLE;
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void trk_finish(TrackSmem<N> &T, const TrackArgs &A, int q, int status)
+{
+    const long long pth = T.path[q];
+    A.status[pth] = (uint8_t)status;
+    A.tau[pth] = T.tau_a[q];
+    if (A.stats) {
+        A.stats[4 * pth + 0] = T.steps[q];
+        A.stats[4 * pth + 1] = T.rej[q];
+        A.stats[4 * pth + 2] = T.evals[q];
+        A.stats[4 * pth + 3] = T.fin[q];
+    }
+    T.done_path[q] = pth;
+}
+
+template <int N>
+__global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys S, const TrackArgs A)
+{
+    using G = Geo<N>;
+    constexpr int PTS = G::PTS, WL = G::WL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TrackSmem<N> &T = *reinterpret_cast<TrackSmem<N> *>(smem_raw);
+    Smem<N> &sm = T.s;
+    const int tid = threadIdx.x;
+    const int k = tid / WL, q = tid % WL;
+    const int lane = tid & 31, warp = tid >> 5;
+    const TrackOpts &o = A.o;
+    for (int i = tid; i < 256; i += G::NT) {
+        sm.exptab[i] = __ldg(S.exptab + i);
+        sm.cistab[i] = __ldg(S.cistab + i);
+    }
+    if (tid < WL) {
+        T.done_path[tid] = -1;
+        if (tid < PTS) trk_pop<N>(T, A, tid);
+        else { T.path[tid] = -1; T.refill[tid] = 0; T.phase[tid] = PH_IDLE; }
+        T.acc[tid] = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        // (1) write back finished paths, accept trial points, load new paths, select the query
+        if (tid < N * PTS) {
+            const int qq = tid / N, j = tid % N;
+            if (T.acc[qq]) T.xa[j][qq] = T.xt[j][qq];
+            if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
+            if (T.refill[qq]) T.xa[j][qq] = A.x[T.path[qq] * N + j];
+            const int ph = T.phase[qq];
+            sm.xs[j][qq] = (ph == PH_CORRECT) ? T.xt[j][qq] : (ph == PH_IDLE ? make_double2(1.0, 0.0) : T.xa[j][qq]);
+        }
+        __syncthreads();
+        if (tid < WL) {
+            T.done_path[tid] = -1;
+            T.acc[tid] = 0;
+            T.refill[tid] = 0;
+            sm.st[tid] = 0;
+            const int ph = (tid < PTS) ? T.phase[tid] : PH_IDLE;
+            sm.tau[tid] = (ph == PH_CORRECT) ? T.tau_t[tid] : ((ph == PH_PREDICT) ? T.tau_a[tid] : 0.0);
+            if (tid >= PTS)
+                for (int j = 0; j < N; ++j) sm.xs[j][tid] = make_double2(1.0, 0.0);
+        }
+        if (tid == 0) T.active = 0;
+        __syncthreads();
+        // (2) evaluation + solve at the query points (same code as pht_pc_step)
+        stage1<N, MODE_STEP>(sm, tid);
+        if (tid < WL && tid >= PTS)
+            for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
+        __syncthreads();
+        if (k < N) {
+            double2 row[N + 2];
+            int e;
+            eval_row<N>(S, sm, k, q, row, e);
+            if (q < PTS) store_row<N>(sm, k, q, row);
+        }
+        __syncthreads();
+        for (int g = warp; g < G::NGRP; g += G::NWARP) {
+            int col, qq;
+            double2 dE, dN;
+            bool sing, act;
+            lsolve<N>(sm, lane, warp, g, col, dE, dN, sing, act, qq);
+            if (act) {
+                if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
+                T.dd[col][qq] = (T.phase[qq] == PH_PREDICT) ? dE : dN;
+            }
+        }
+        __syncthreads();
+        // (3) element-parallel updates
+        if (tid < N * PTS) {
+            const int qq = tid / N, j = tid % N;
+            const int ph = T.phase[qq];
+            if (sm.st[qq] == 0 && ph != PH_IDLE) {
+                if (ph == PH_PREDICT) {
+                    const double h = fmin(T.dt[qq], -T.tau_a[qq]);
+                    const double2 xv = T.xa[j][qq], d = cmul(xv, T.dd[j][qq]);
+                    T.xt[j][qq] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
+                } else if (ph == PH_CORRECT) {
+                    const double2 xv = T.xt[j][qq], dl = T.dd[j][qq], d = cmul(xv, dl);
+                    T.xt[j][qq] = make_double2(xv.x + d.x, xv.y + d.y);
+                    T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_j / x_j|^2 (reading R14)
+                } else { // FINAL
+                    const double2 xv = T.xa[j][qq], dl = T.dd[j][qq], d = cmul(xv, dl);
+                    T.xa[j][qq] = make_double2(xv.x + d.x, xv.y + d.y);
+                    T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y);
+                }
+            }
+        }
+        __syncthreads();
+        // (4) per-slot decisions (the oracle's control flow, oracle.c orc_track)
+        if (tid < PTS && T.phase[tid] != PH_IDLE) {
+            const int qq = tid;
+            const int ph = T.phase[qq];
+            const int bad = sm.st[qq];
+            T.evals[qq] += 1;
+            int finish = -1; // status when the path ends this iteration
+            bool reject = false;
+            if (ph == PH_PREDICT) {
+                if (bad) reject = true;
+                else {
+                    T.tau_t[qq] = T.tau_a[qq] + fmin(T.dt[qq], -T.tau_a[qq]);
+                    T.phase[qq] = PH_CORRECT;
+                    T.it[qq] = 1;
+                    T.prev[qq] = INFINITY;
+                }
+            } else if (ph == PH_CORRECT) {
+                if (bad) reject = true;
+                else {
+                    double nd = 0.0; // max_j |dx_j| / |x_j| (componentwise relative, reading R14)
+                    for (int j = 0; j < N; ++j) nd = fmax(nd, T.nd2[j][qq]);
+                    nd = sqrt(nd);
+                    if (nd <= o.newton_tol) {
+                        T.acc[qq] = 1;
+                        T.tau_a[qq] = T.tau_t[qq];
+                        T.steps[qq] += 1;
+                        if (++T.succ[qq] == o.grow_after) { T.dt[qq] = fmin(o.grow * T.dt[qq], o.dtau_max); T.succ[qq] = 0; }
+                        T.phase[qq] = (T.tau_a[qq] < 0.0) ? PH_PREDICT : PH_FINAL;
+                        if (T.phase[qq] == PH_PREDICT && T.steps[qq] == o.max_steps) finish = 16; // MAX_STEPS
+                    } else if ((T.it[qq] >= 2 && nd > 0.5 * T.prev[qq]) || T.it[qq] >= o.K) {
+                        reject = true;
+                    } else {
+                        T.prev[qq] = nd;
+                        T.it[qq] += 1;
+                    }
+                }
+            } else { // FINAL
+                T.fin[qq] += 1;
+                if (bad) finish = 32;
+                else {
+                    double nd = 0.0, xinf = 0.0;
+                    for (int j = 0; j < N; ++j) {
+                        nd = fmax(nd, T.nd2[j][qq]);
+                        const double2 v = T.xa[j][qq];
+                        xinf = fmax(xinf, sqrt(fma(v.x, v.x, v.y * v.y)));
+                    }
+                    if (sqrt(nd) <= o.final_tol) finish = (xinf <= o.inf_norm) ? 0 : 32;
+                    else if (T.fin[qq] >= o.final_iters) finish = 32;
+                }
+            }
+            if (reject) {
+                T.rej[qq] += 1;
+                T.dt[qq] *= o.shrink;
+                T.succ[qq] = 0;
+                if (T.dt[qq] < o.dtau_min) finish = (bad & PT_SINGULAR) ? PT_SINGULAR : 8; // STEP_UNDERFLOW
+                else {
+                    T.phase[qq] = PH_PREDICT;
+                    if (T.steps[qq] == o.max_steps) finish = 16;
+                }
+            }
+            if (finish >= 0) {
+                trk_finish<N>(T, A, qq, finish);
+                trk_pop<N>(T, A, qq);
+            }
+            if (T.phase[qq] != PH_IDLE) atomicAdd(&T.active, 1);
+        }
+        __syncthreads();
+        if (T.active == 0) {
+            // flush the last finished paths
+            if (tid < N * PTS) {
+                const int qq = tid / N, j = tid % N;
+                if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
+            }
+            break;
+        }
+    }
+}
+
+template <int N>
+cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+{
+    const size_t sb = sizeof(TrackSmem<N>);
+    static std::atomic<unsigned long long> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(k_track<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        if (e != cudaSuccess) return e;
+        configured.fetch_or(bit);
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track<N>, Geo<N>::NT, sb);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sms * per_sm;
+    const int64_t need = (A.P + Geo<N>::PTS - 1) / Geo<N>::PTS;
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    k_track<N><<<dim3((unsigned)grid), dim3(Geo<N>::NT), sb, stream>>>(S, A);
+    return cudaGetLastError();
 }
 
 template <int N, int MODE>

@@ -1,0 +1,99 @@
+"""GPU tracker (pht_track) parity against the oracle tracker (oracle.c orc_track).
+
+Bar (BASELINE.json north_star): endpoints agree to <= 1e-8 and the count of finite solutions is
+identical.  Accept/reject decisions may flip at rounding level (reading R14), so step counts are
+compared as statistics, not per path."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from workloads import startsys as SS
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2111_14317_b200 as P
+    return P
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _run_gpu(P, sysm, x, tau, **opts):
+    g = P.System.from_workload(sysm)
+    xd, td = _cuda(x), _cuda(tau)
+    st, stats = g.track(xd, td, **opts)
+    return xd.cpu().numpy(), td.cpu().numpy(), st.cpu().numpy(), stats.cpu().numpy()
+
+
+def test_track_diagonal_closed_form(P):
+    d, b, w = [2, 3, 1], [0.5 + 1j, -2.0, 1j], [3, 5, 2]
+    sysm = W.diagonal(d, b, w)
+    tau0 = -4.0
+    t0 = np.exp(tau0)
+    r0 = [np.roots([1] + [0] * (d[k] - 1) + [-b[k] * t0 ** w[k]]) for k in range(3)]
+    starts = np.array([[u, v, s] for u in r0[0] for v in r0[1] for s in r0[2]], np.complex128)
+    xg, tg, sg, stg = _run_gpu(P, sysm, starts, np.full(len(starts), tau0))
+    xo, to, so, sto = oracle.Oracle(sysm).track(starts, np.full(len(starts), tau0))
+    assert np.all(sg == 0) and np.all(so == 0) and np.all(tg == 0)
+    assert np.max(np.abs(xg - xo) / np.abs(xo)) <= 1e-8
+    roots = [np.roots([1] + [0] * (d[k] - 1) + [-b[k]]) for k in range(3)]
+    for k in range(3):
+        assert np.all(np.min(np.abs(xg[:, k][:, None] - roots[k][None, :]), axis=1) < 1e-12)
+
+
+def test_track_cyclic5_all_70_paths(P):
+    c5 = W.cyclic(5, lift_max=100)
+    x, tau0, _, _ = SS.start_points(c5, zmax=20)
+    xg, tg, sg, stg = _run_gpu(P, c5, x, tau0)
+    xo, to, so, sto = oracle.Oracle(c5).track(x, tau0)
+    assert np.sum(sg == 0) == np.sum(so == 0) == 70
+    rel = np.linalg.norm(xg - xo, axis=1) / np.linalg.norm(xo, axis=1)
+    assert rel.max() <= 1e-8, rel.max()
+    # finite-solution count and distinctness
+    assert len({tuple(np.round(v, 7)) for v in xg}) == 70
+    # effort statistics agree (decisions may flip at rounding level)
+    assert abs(stg[:, 0].sum() - sto[:, 0].sum()) <= 0.02 * sto[:, 0].sum() + 5
+    r = oracle.Oracle(c5).evaluate(xg, np.ones(70))
+    assert np.max(np.abs(r["H"]) / r["SH"]) < 1e-13
+
+
+def test_track_deterministic_and_order_invariant(P):
+    c5 = W.cyclic(5, lift_max=100)
+    x, tau0, _, _ = SS.start_points(c5, zmax=20)
+    perm = np.random.default_rng(0).permutation(len(x))
+    xa, ta, sa, _ = _run_gpu(P, c5, x, tau0)
+    xb, tb, sb, _ = _run_gpu(P, c5, x[perm], tau0[perm])
+    assert np.array_equal(xa[perm], xb) and np.array_equal(sa[perm], sb)
+
+
+def test_track_status_isolation(P):
+    """batch of 8 with one poisoned start -> 7 converge."""
+    sysm = W.from_terms("lin", 1, [[((1,), 1.0, 0), ((0,), -1.0, 1)]], coeffs="native")
+    starts = np.full((8, 1), np.exp(-5.0) + 0j)
+    starts[3, 0] = 0
+    tau = np.full(8, -5.0)
+    tau[6] = np.nan
+    xg, tg, sg, _ = _run_gpu(P, sysm, starts, tau)
+    assert sg[3] != 0 and sg[6] == P.PT_NONFINITE and np.sum(sg == 0) == 6
+    assert np.allclose(xg[sg == 0, 0], 1.0, atol=1e-13)
+
+
+def test_track_many_slots_queue(P):
+    """More paths than resident slots: the atomic queue hands every path out exactly once."""
+    d, b, w = [2, 2], [0.3 + 0.4j, 1.5j], [4, 7]
+    sysm = W.diagonal(d, b, w)
+    tau0 = -3.0
+    t0 = np.exp(tau0)
+    r0 = [np.roots([1, 0, -b[k] * t0 ** w[k]]) for k in range(2)]
+    base = np.array([[u, v] for u in r0[0] for v in r0[1]], np.complex128)
+    starts = np.tile(base, (5000, 1))
+    xg, tg, sg, stg = _run_gpu(P, sysm, starts, np.full(len(starts), tau0))
+    assert np.all(sg == 0)
+    ref = xg[:4]
+    assert np.array_equal(xg, np.tile(ref, (5000, 1)))

@@ -1,0 +1,176 @@
+"""Start points of the polyhedral homotopy for small systems (workload preparation).
+
+The paper assumes the start points are given ("we simply assume the set of all
+solutions to H(x, t0) = 0 ... is readily available").  This module produces them the standard
+way (Huber-Sturmfels), for SMALL systems only (brute force over edge tuples):
+
+1. Fine mixed cells: one pair {a_k, a'_k} of S_k per equation with an inner normal (alpha, 1):
+   <a_k, alpha> + w(a_k) = <a'_k, alpha> + w(a'_k) = beta_k  and  <b, alpha> + w(b) > beta_k
+   for every other b in S_k.  Exact rational arithmetic.  Volume |det V|, V = [a_k - a'_k]_k.
+2. Binomial start system per cell: c_k y^{a_k} + c'_k y^{a'_k} = 0  <=>  y^{V} = -c'/c, solved in
+   log coordinates via a Hermite normal form U V = T (all |det V| branches).
+3. Start point on the path at tau0 (per cell): x = exp(tau0 alpha + log y), tau0 = -L / gap with
+   gap = the smallest lifting gap of the cell, so the neglected terms are O(e^{-L}).
+
+No evaluation of H or its derivatives happens here (nothing of the method's arithmetic).
+"""
+from __future__ import annotations
+
+import itertools
+from fractions import Fraction
+from typing import List, Tuple
+
+import numpy as np
+
+
+def _solve_rational(V: List[List[int]], b: List[Fraction]):
+    """Gaussian elimination over Q; returns x or None if singular."""
+    n = len(V)
+    M = [[Fraction(V[i][j]) for j in range(n)] + [Fraction(b[i])] for i in range(n)]
+    for c in range(n):
+        p = next((r for r in range(c, n) if M[r][c] != 0), None)
+        if p is None:
+            return None
+        M[c], M[p] = M[p], M[c]
+        for r in range(n):
+            if r != c and M[r][c] != 0:
+                f = M[r][c] / M[c][c]
+                M[r] = [M[r][j] - f * M[c][j] for j in range(n + 1)]
+    return [M[i][n] / M[i][i] for i in range(n)]
+
+
+def _det_int(V: List[List[int]]) -> int:
+    M = [[Fraction(v) for v in row] for row in V]
+    n = len(M)
+    det = Fraction(1)
+    for c in range(n):
+        p = next((r for r in range(c, n) if M[r][c] != 0), None)
+        if p is None:
+            return 0
+        if p != c:
+            M[c], M[p] = M[p], M[c]
+            det = -det
+        det *= M[c][c]
+        for r in range(c + 1, n):
+            f = M[r][c] / M[c][c]
+            M[r] = [M[r][j] - f * M[c][j] for j in range(n)]
+    return int(det)
+
+
+def mixed_cells(system) -> List[dict]:
+    """All fine mixed cells of the lifted supports (brute force over pair tuples)."""
+    n = system.n
+    sup = []
+    for k in range(n):
+        rows = [(tuple(int(v) for v in system.exps[i]), Fraction(system.lifting[i]).limit_denominator(10**9), i)
+                for i in system.terms_of(k)]
+        sup.append(rows)
+    cells = []
+    for pairs in itertools.product(*[list(itertools.combinations(range(len(s)), 2)) for s in sup]):
+        V = [[sup[k][pairs[k][0]][0][j] - sup[k][pairs[k][1]][0][j] for j in range(n)] for k in range(n)]
+        rhs = [sup[k][pairs[k][1]][1] - sup[k][pairs[k][0]][1] for k in range(n)]
+        alpha = _solve_rational(V, rhs)
+        if alpha is None:
+            continue
+        ok = True
+        gap = None
+        for k in range(n):
+            a0, w0, _ = sup[k][pairs[k][0]]
+            beta = sum(Fraction(a0[j]) * alpha[j] for j in range(n)) + w0
+            for idx, (b, wb, _) in enumerate(sup[k]):
+                if idx in pairs[k]:
+                    continue
+                d = sum(Fraction(b[j]) * alpha[j] for j in range(n)) + wb - beta
+                if d <= 0:
+                    ok = False
+                    break
+                gap = d if gap is None else min(gap, d)
+            if not ok:
+                break
+        if not ok:
+            continue
+        cells.append({"pairs": [(sup[k][pairs[k][0]][2], sup[k][pairs[k][1]][2]) for k in range(n)],
+                      "V": V, "alpha": alpha, "gap": gap, "volume": abs(_det_int(V))})
+    return cells
+
+
+def mixed_volume(system) -> int:
+    return sum(c["volume"] for c in mixed_cells(system))
+
+
+def _hnf_rows(V: List[List[int]]) -> Tuple[List[List[int]], List[List[int]]]:
+    """Row-style Hermite reduction: unimodular U with U V = T upper triangular."""
+    n = len(V)
+    T = [list(r) for r in V]
+    U = [[int(i == j) for j in range(n)] for i in range(n)]
+    r = 0
+    for c in range(n):
+        # Euclid on column c among rows r..n-1
+        while True:
+            nz = [i for i in range(r, n) if T[i][c] != 0]
+            if len(nz) <= 1:
+                break
+            p = min(nz, key=lambda i: abs(T[i][c]))
+            for i in nz:
+                if i != p:
+                    q = T[i][c] // T[p][c]
+                    T[i] = [T[i][j] - q * T[p][j] for j in range(n)]
+                    U[i] = [U[i][j] - q * U[p][j] for j in range(n)]
+        nz = [i for i in range(r, n) if T[i][c] != 0]
+        if not nz:
+            continue
+        p = nz[0]
+        T[r], T[p] = T[p], T[r]
+        U[r], U[p] = U[p], U[r]
+        if T[r][c] < 0:
+            T[r] = [-v for v in T[r]]
+            U[r] = [-v for v in U[r]]
+        r += 1
+    return U, T
+
+
+def cell_start_points(system, cell, L: float = 37.0, tau_cap: float | None = None,
+                      zmax: float | None = None):
+    """All |det V| start points of one cell: returns (x [vol, n] complex128, tau0, z [vol, n]).
+
+    tau0 = -L / gap (neglected terms O(e^{-L})), optionally capped so that |tau0| <= tau_cap
+    and |tau0 * alpha_j| <= zmax (keeps |x| inside double range at the price of a larger start
+    residual, which the tracker's first corrections remove)."""
+    n = system.n
+    V = cell["V"]
+    U, T = _hnf_rows(V)
+    c = system.coeffs
+    logb = np.array([np.log(-c[j1] / c[j0]) for (j0, j1) in cell["pairs"]], np.complex128)
+    w = np.array([sum(U[k][l] * logb[l] for l in range(n)) for k in range(n)], np.complex128)
+    sols = [np.zeros(n, np.complex128)]
+    for row in range(n - 1, -1, -1):
+        new = []
+        d = T[row][row]
+        for z in sols:
+            rest = w[row] - sum(T[row][j] * z[j] for j in range(row + 1, n))
+            for m in range(abs(d)):
+                zz = z.copy()
+                zz[row] = (rest + 2j * np.pi * m) / d
+                new.append(zz)
+        sols = new
+    Z = np.array(sols)
+    alpha = np.array([float(a) for a in cell["alpha"]])
+    tau0 = -L / float(cell["gap"])
+    if tau_cap is not None:
+        tau0 = max(tau0, -tau_cap)
+    if zmax is not None and np.max(np.abs(alpha)) > 0:
+        tau0 = max(tau0, -zmax / float(np.max(np.abs(alpha))))
+    Zt = Z + tau0 * alpha[None, :]
+    return np.exp(Zt), tau0, Zt
+
+
+def start_points(system, L: float = 37.0, tau_cap: float | None = None, zmax: float | None = None):
+    """Start points of every mixed cell: (x [MV, n], tau0 [MV], cell id [MV], z [MV, n])."""
+    xs, taus, ids, zs = [], [], [], []
+    for ci, cell in enumerate(mixed_cells(system)):
+        x, t0, z = cell_start_points(system, cell, L, tau_cap, zmax)
+        xs.append(x)
+        zs.append(z)
+        taus.append(np.full(len(x), t0))
+        ids.append(np.full(len(x), ci))
+    return (np.concatenate(xs), np.concatenate(taus), np.concatenate(ids), np.concatenate(zs))
