@@ -75,3 +75,19 @@ def test_oracle_tracker_finds_all_cyclic5_solutions():
     r = o.evaluate(xe, np.ones(70))
     assert np.max(np.abs(r["H"]) / r["SH"]) < 1e-13
     assert len({tuple(np.round(v, 7)) for v in xe}) == 70
+
+
+def test_fast_enumerator_equals_brute_force():
+    """The LP-pruned C++ enumerator (workloads/mixedcell.cpp) finds exactly the brute-force cells."""
+    for sysm in (W.cyclic(5, lift_max=100), W.cyclic(4, lift_max=1000), W.noon(3, lift_max=100),
+                 W.katsura(3, lift_max=100), W.random_dense(3, 5, seed=4, lift_max=10**4)):
+        a = {tuple(c["pairs"]) for c in SS.mixed_cells(sysm)}
+        b = {tuple(c["pairs"]) for c in SS.mixed_cells_fast(sysm)}
+        assert a == b, sysm.name
+
+
+def test_known_mixed_volumes():
+    """Published torus root counts [ext]: noon-n = 3^n - 2n, cyclic-7 = 924 (generic lifting)."""
+    assert sum(c["volume"] for c in SS.mixed_cells_fast(W.noon(4, lift_max=1000))) == 3 ** 4 - 8
+    assert sum(c["volume"] for c in SS.mixed_cells_fast(W.noon(5, lift_max=1000))) == 3 ** 5 - 10
+    assert sum(c["volume"] for c in SS.mixed_cells_fast(W.cyclic(7, lift_max=10 ** 4))) == 924

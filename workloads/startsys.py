@@ -94,6 +94,58 @@ def mixed_cells(system) -> List[dict]:
     return cells
 
 
+def mixed_cells_fast(system, max_cells: int = 2_000_000) -> List[dict]:
+    """Same cells as mixed_cells(), via the C++ enumerator (lower edges, pairwise compatibility,
+    LP-pruned depth-first search; workloads/mixedcell.cpp).  Cell records carry exact rational
+    alpha/gap recomputed from the pairs."""
+    import ctypes
+    import os
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    lib_path = os.path.join(here, "libmixedcell.so")
+    src = os.path.join(here, "mixedcell.cpp")
+    if not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", here, "libmixedcell.so"], check=True)
+    lib = ctypes.CDLL(lib_path)
+    lib.mc_cells.restype = ctypes.c_int64
+    n = system.n
+    off = np.ascontiguousarray(system.offsets, np.int64)
+    ex = np.ascontiguousarray(system.exps, np.int32)
+    lift = np.ascontiguousarray(system.lifting, np.float64)
+    pairs = np.zeros((max_cells, n, 2), np.int32)
+    alpha = np.zeros((max_cells, n))
+    gap = np.zeros(max_cells)
+    stats = np.zeros(4, np.int64)
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    cnt = lib.mc_cells(ctypes.c_int(n), P(off), P(ex), P(lift), ctypes.c_int64(max_cells), P(pairs), P(alpha),
+                       P(gap), P(stats))
+    if cnt < 0:
+        raise RuntimeError("too many mixed cells")
+    cells = []
+    for c in range(cnt):
+        pr = [(int(pairs[c, k, 0]), int(pairs[c, k, 1])) for k in range(n)]
+        V = [[int(system.exps[p][j]) - int(system.exps[q][j]) for j in range(n)] for (p, q) in pr]
+        rhs = [Fraction(system.lifting[q]).limit_denominator(10**9) - Fraction(system.lifting[p]).limit_denominator(10**9)
+               for (p, q) in pr]
+        al = _solve_rational(V, rhs)
+        g = None
+        for k in range(n):
+            p0, q0 = pr[k]
+            beta = sum(Fraction(int(system.exps[p0][j])) * al[j] for j in range(n)) + \
+                Fraction(system.lifting[p0]).limit_denominator(10**9)
+            for i in system.terms_of(k):
+                if i in (p0, q0):
+                    continue
+                d = sum(Fraction(int(system.exps[i][j])) * al[j] for j in range(n)) + \
+                    Fraction(system.lifting[i]).limit_denominator(10**9) - beta
+                if d <= 0:
+                    raise RuntimeError("enumerated cell fails the exact check")
+                g = d if g is None else min(g, d)
+        cells.append({"pairs": pr, "V": V, "alpha": al, "gap": g, "volume": abs(_det_int(V))})
+    mixed_cells_fast.last_stats = stats.copy()
+    return cells
+
+
 def mixed_volume(system) -> int:
     return sum(c["volume"] for c in mixed_cells(system))
 
@@ -164,10 +216,12 @@ def cell_start_points(system, cell, L: float = 37.0, tau_cap: float | None = Non
     return np.exp(Zt), tau0, Zt
 
 
-def start_points(system, L: float = 37.0, tau_cap: float | None = None, zmax: float | None = None):
+def start_points(system, L: float = 37.0, tau_cap: float | None = None, zmax: float | None = None,
+                 fast: bool = False):
     """Start points of every mixed cell: (x [MV, n], tau0 [MV], cell id [MV], z [MV, n])."""
     xs, taus, ids, zs = [], [], [], []
-    for ci, cell in enumerate(mixed_cells(system)):
+    cells = mixed_cells_fast(system) if fast else mixed_cells(system)
+    for ci, cell in enumerate(cells):
         x, t0, z = cell_start_points(system, cell, L, tau_cap, zmax)
         xs.append(x)
         zs.append(z)
