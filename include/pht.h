@@ -152,7 +152,8 @@ int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
  * corrections, accept -> grow dtau by `grow` after `grow_after` successes, reject -> shrink),
  * lands exactly on tau = 0, then refines with up to final_iters Newton steps at t = 1;
  * finished slots take the next path from an atomic queue.
- *   x       c128[p][n] start points in (on their paths at tau), endpoints out.
+ *   x       c128[p][n] start points in (on their paths at tau), endpoints out (z = log x
+ *           instead of x when opts->log_state).
  *   tau     double[p] start parameters tau0 <= 0 in; final tau (0 when tracked) out.
  *   opts    options; NULL = defaults (pht_track_opts_default).
  *   stats   int64[p][4] or NULL: accepted steps, rejected steps, evaluations (each one
@@ -175,6 +176,9 @@ typedef struct {
     int32_t grow_after;   /* 3                                                           */
     int32_t max_steps;    /* 10000                                                       */
     int32_t final_iters;  /* 5                                                           */
+    int32_t log_state;    /* 0: x holds points x; 1: x holds z = log x (any branch) — for start
+                             points far outside double range (|Re z| > ~700); the steps are the
+                             same affine updates, applied as z <- z + log(1 + dx/x)            */
 } pht_track_opts;
 
 void pht_track_opts_default(pht_track_opts *opts);

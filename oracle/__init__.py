@@ -150,6 +150,38 @@ class Oracle:
         return x, tau, st, stats
 
 
+    def track_x(self, xm, xe, tau, *, dtau_init=0.05, dtau_min=1e-8, dtau_max=0.5, newton_tol=1e-10,
+                shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
+                max_steps=10000, final_iters=5):
+        """orc_track_x: the tracker with extended-range state x = xm * 2**xe."""
+        xm = _c2(xm).copy()
+        xe = np.ascontiguousarray(xe, np.int64).copy()
+        tau = np.ascontiguousarray(tau, np.float64).copy()
+        p = xm.shape[0]
+        opt = np.array([dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm])
+        iopt = np.array([K, grow_after, max_steps, final_iters], np.int32)
+        st = np.zeros(p, np.uint8)
+        stats = np.zeros((p, 4), np.int64)
+        rc = lib().orc_track_x(*self._sys_args(), ctypes.c_int64(p), _p(xm), _p(xe), _p(tau), _p(opt),
+                               _p(iopt), _p(st), _p(stats))
+        assert rc == 0
+        return xm, xe, tau, st, stats
+
+
+# --- test plumbing (not the oracle): log coordinates <-> extended-range (mantissa, exponent) ---
+def z_to_x(z):
+    """z = log x  ->  (m, e) with x = m * 2**e, |m| in [1, 2)."""
+    z = np.asarray(z, np.complex128)
+    e = np.floor(z.real / np.log(2)).astype(np.int64)
+    m = np.exp(z.real - e * np.log(2)) * np.exp(1j * z.imag)
+    return m, e
+
+
+def x_to_z(m, e):
+    """(m, e) -> z = log m + e ln 2 (principal branch of log m)."""
+    return np.log(np.asarray(m, np.complex128)) + np.asarray(e, np.float64) * np.log(2)
+
+
 def lu_solve(A, B):
     """Route 1 (Gaussian elimination, partial pivoting): returns (X, status)."""
     A = _c2(A)

@@ -29,6 +29,8 @@
  *                     Newton iterations.
  *   orc_track         adaptive predictor-corrector tracking tau0 -> 0 (SURVEY §8(c) O4,
  *                     step control = DESIGN.md reading R14).
+ *   orc_track_x       the same tracker with extended-range state for start points far outside
+ *                     double range (polyhedral start points at large |tau0|).
  *
  * All complex numbers are interleaved (re, im) doubles.  Arithmetic is plain C
  * double in a fixed order; OpenMP only distributes independent points/paths.
@@ -262,6 +264,61 @@ static double xabs_log2(xc a) /* log2 |a|, for the scale sums */
     return m == 0.0 ? -INFINITY : log2(m) + (double)a.e;
 }
 
+/*
+ * Extended-range evaluation of one point (the same definition as eval_point):
+ * x[j], t as xc values; outputs H[k], Jx[k*n+j], Jt[k] and the absolute term sums (xc).
+ */
+static void eval_point_x(const orc_sys *s, const xc *x, xc t, xc *H, xc *Jx, xc *Jt,
+                         xc *SH, xc *SJx, xc *SJt)
+{
+    const int n = s->n;
+    xc r[64];
+    for (int j = 0; j < n; ++j) r[j] = xinv(x[j]);
+    for (int k = 0; k < n; ++k) {
+        xc h = {0, 0}, ht = {0, 0}, hx[64];
+        xc sh = {0, 0}, sht = {0, 0}, shx[64];
+        for (int j = 0; j < n; ++j) { hx[j].m = 0; hx[j].e = 0; shx[j].m = 0; shx[j].e = 0; }
+        for (int64_t i = s->off[k]; i < s->off[k + 1]; ++i) {
+            const int32_t *ai = s->a + i * n;
+            xc cc = xnorm(load(s->c + 2 * i), 0);
+            xc tw = xpow_nat(t, s->w[i]);
+            xc T = cc;
+            for (int j = 0; j < n; ++j)
+                if (ai[j] != 0) T = xmul(T, ai[j] > 0 ? xpow_nat(x[j], ai[j]) : xpow_nat(r[j], -ai[j]));
+            T = xmul(T, tw);
+            h = xadd(h, T);
+            sh = xadd(sh, xnorm(mk(cabs(T.m), 0), T.e));
+            for (int j = 0; j < n; ++j) {
+                if (ai[j] == 0) continue;
+                xc D = xmul(cc, xnorm(mk((double)ai[j], 0), 0));
+                for (int l = 0; l < n; ++l) {
+                    int64_t e = ai[l] - (l == j ? 1 : 0);
+                    if (e != 0) D = xmul(D, e > 0 ? xpow_nat(x[l], e) : xpow_nat(r[l], -e));
+                }
+                D = xmul(D, tw);
+                hx[j] = xadd(hx[j], D);
+                shx[j] = xadd(shx[j], xnorm(mk(cabs(D.m), 0), D.e));
+            }
+            if (s->w[i] >= 1) {
+                xc D = xmul(cc, xnorm(mk((double)s->w[i], 0), 0));
+                for (int j = 0; j < n; ++j)
+                    if (ai[j] != 0) D = xmul(D, ai[j] > 0 ? xpow_nat(x[j], ai[j]) : xpow_nat(r[j], -ai[j]));
+                D = xmul(D, xpow_nat(t, s->w[i] - 1));
+                ht = xadd(ht, D);
+                sht = xadd(sht, xnorm(mk(cabs(D.m), 0), D.e));
+            }
+        }
+        H[k] = h;
+        Jt[k] = ht;
+        if (SH) SH[k] = sh;
+        if (SJt) SJt[k] = sht;
+        for (int j = 0; j < n; ++j) {
+            Jx[k * n + j] = hx[j];
+            if (SJx) SJx[k * n + j] = shx[j];
+        }
+    }
+}
+
 /* x_j = xm_j * 2^{xe_j}, t = tm * 2^{te}; outputs as (mantissa, exponent) pairs and the
  * log2 of the absolute term sums (LSH etc.) for the parity metric. */
 int orc_evaluate_x(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
@@ -270,58 +327,23 @@ int orc_evaluate_x(int n, const int64_t *off, const int32_t *a, const double *c,
                    double *Jtm, int64_t *Jte, double *LSH, double *LSJx, double *LSJt)
 {
     if (n < 1 || n > 64) return -1;
+    orc_sys s = {n, off, a, c, w};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t q = 0; q < p; ++q) {
-        xc x[64], r[64], t;
-        for (int j = 0; j < n; ++j) {
-            x[j] = xnorm(load(xm + 2 * (q * n + j)), xe[q * n + j]);
-            r[j] = xinv(x[j]);
-        }
-        t = xnorm(mk(tm[q], 0.0), te[q]);
+        xc x[64], H[64], Jx[64 * 64], Jt[64], SH[64], SJx[64 * 64], SJt[64];
+        for (int j = 0; j < n; ++j) x[j] = xnorm(load(xm + 2 * (q * n + j)), xe[q * n + j]);
+        xc t = xnorm(mk(tm[q], 0.0), te[q]);
+        eval_point_x(&s, x, t, H, Jx, Jt, SH, SJx, SJt);
         for (int k = 0; k < n; ++k) {
-            xc h = {0, 0}, ht = {0, 0}, hx[64];
-            /* log2 of running absolute sums, accumulated in extended range too */
-            xc sh = {0, 0}, sht = {0, 0}, shx[64];
-            for (int j = 0; j < n; ++j) { hx[j].m = 0; hx[j].e = 0; shx[j].m = 0; shx[j].e = 0; }
-            for (int64_t i = off[k]; i < off[k + 1]; ++i) {
-                const int32_t *ai = a + i * n;
-                xc cc = xnorm(load(c + 2 * i), 0);
-                xc tw = xpow_nat(t, w[i]);
-                xc T = cc;
-                for (int j = 0; j < n; ++j)
-                    if (ai[j] != 0) T = xmul(T, ai[j] > 0 ? xpow_nat(x[j], ai[j]) : xpow_nat(r[j], -ai[j]));
-                T = xmul(T, tw);
-                h = xadd(h, T);
-                sh = xadd(sh, xnorm(mk(cabs(T.m), 0), T.e));
-                for (int j = 0; j < n; ++j) {
-                    if (ai[j] == 0) continue;
-                    xc D = xmul(cc, xnorm(mk((double)ai[j], 0), 0));
-                    for (int l = 0; l < n; ++l) {
-                        int64_t e = ai[l] - (l == j ? 1 : 0);
-                        if (e != 0) D = xmul(D, e > 0 ? xpow_nat(x[l], e) : xpow_nat(r[l], -e));
-                    }
-                    D = xmul(D, tw);
-                    hx[j] = xadd(hx[j], D);
-                    shx[j] = xadd(shx[j], xnorm(mk(cabs(D.m), 0), D.e));
-                }
-                if (w[i] >= 1) {
-                    xc D = xmul(cc, xnorm(mk((double)w[i], 0), 0));
-                    for (int j = 0; j < n; ++j)
-                        if (ai[j] != 0) D = xmul(D, ai[j] > 0 ? xpow_nat(x[j], ai[j]) : xpow_nat(r[j], -ai[j]));
-                    D = xmul(D, xpow_nat(t, w[i] - 1));
-                    ht = xadd(ht, D);
-                    sht = xadd(sht, xnorm(mk(cabs(D.m), 0), D.e));
-                }
-            }
             int64_t o = q * n + k;
-            store(Hm + 2 * o, h.m); He[o] = h.e;
-            store(Jtm + 2 * o, ht.m); Jte[o] = ht.e;
-            LSH[o] = xabs_log2(sh);
-            LSJt[o] = xabs_log2(sht);
+            store(Hm + 2 * o, H[k].m); He[o] = H[k].e;
+            store(Jtm + 2 * o, Jt[k].m); Jte[o] = Jt[k].e;
+            LSH[o] = xabs_log2(SH[k]);
+            LSJt[o] = xabs_log2(SJt[k]);
             for (int j = 0; j < n; ++j) {
-                int64_t oo = (q * n + k) * n + j;
-                store(Jxm + 2 * oo, hx[j].m); Jxe[oo] = hx[j].e;
-                LSJx[oo] = xabs_log2(shx[j]);
+                int64_t oo = o * n + j;
+                store(Jxm + 2 * oo, Jx[k * n + j].m); Jxe[oo] = Jx[k * n + j].e;
+                LSJx[oo] = xabs_log2(SJx[k * n + j]);
             }
         }
     }
@@ -628,6 +650,159 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             for (int j = 0; j < n; ++j) xinf = fmax(xinf, cabs(load(xq + 2 * j)));
             st = (conv && xinf <= inf_norm) ? ORC_PT_OK : ORC_PT_DIVERGED;
         }
+        tau[q] = tq;
+        status[q] = (uint8_t)st;
+        stats[4 * q + 0] = steps;
+        stats[4 * q + 1] = rejects;
+        stats[4 * q + 2] = evals;
+        stats[4 * q + 3] = fin;
+    }
+    return 0;
+}
+
+
+/* t = e^tau as an extended-range value (Eq. (2)): t = 2^e * exp(tau - e ln 2). */
+static xc xexp_real(double tau)
+{
+    const double L2 = 0.69314718055994530942;
+    double e = floor(tau / L2);
+    return xnorm(mk(exp(tau - e * L2), 0.0), (int64_t)e);
+}
+
+/* Extended-range direction solve at (x, tau): rows [D_z h_k | t dh_k/dt | h_k] with
+ * D_z h = Jx diag(x), each row divided by its largest binary exponent (row
+ * scaling leaves the solution unchanged), then LU in double:
+ * D_z H delta_E = -dH/dtau, D_z H delta_N = -H (dx = x (.) delta). */
+static int solve_point_x(const orc_sys *s, const xc *x, double tau, double *dEr, double *dNr)
+{
+    const int n = s->n;
+    xc H[64], Jx[64 * 64], Jt[64];
+    xc t = xexp_real(tau);
+    for (int j = 0; j < n; ++j)
+        if (creal(x[j].m) == 0.0 && cimag(x[j].m) == 0.0) return ORC_PT_ZERO_COORD;
+    eval_point_x(s, x, t, H, Jx, Jt, 0, 0, 0);
+    double A[64 * 64 * 2], B[64 * 2 * 2], X[64 * 2 * 2];
+    for (int k = 0; k < n; ++k) {
+        xc row[66];
+        for (int j = 0; j < n; ++j) row[j] = xmul(Jx[k * n + j], x[j]);
+        row[n] = xmul(Jt[k], t);
+        row[n + 1] = H[k];
+        int64_t emax = INT64_MIN;
+        for (int j = 0; j < n + 2; ++j)
+            if ((creal(row[j].m) != 0.0 || cimag(row[j].m) != 0.0) && row[j].e > emax) emax = row[j].e;
+        if (emax == INT64_MIN) emax = 0;
+        for (int j = 0; j < n + 2; ++j) {
+            int64_t d = row[j].e - emax;
+            cplx v = d < -1100 ? mk(0.0, 0.0) : mk(ldexp(creal(row[j].m), (int)d), ldexp(cimag(row[j].m), (int)d));
+            if (!isfinite(creal(v)) || !isfinite(cimag(v))) return ORC_PT_NONFINITE;
+            if (j < n) store(A + 2 * (k * n + j), v);
+            else if (j == n) store(B + 2 * (k * 2 + 0), -v);
+            else store(B + 2 * (k * 2 + 1), -v);
+        }
+    }
+    int st = orc_lu_solve(n, 2, A, B, X);
+    if (st) return st;
+    for (int k = 0; k < n; ++k) {
+        if (dEr) { dEr[2 * k] = X[2 * (k * 2)]; dEr[2 * k + 1] = X[2 * (k * 2) + 1]; }
+        if (dNr) { dNr[2 * k] = X[2 * (k * 2 + 1)]; dNr[2 * k + 1] = X[2 * (k * 2 + 1) + 1]; }
+    }
+    for (int k = 0; k < 2 * n; ++k)
+        if ((dEr && !isfinite(dEr[k])) || (dNr && !isfinite(dNr[k]))) return ORC_PT_NONFINITE;
+    return 0;
+}
+
+static double relmax_d(int n, const double *d)
+{
+    double r = 0.0;
+    for (int j = 0; j < n; ++j) {
+        double q = hypot(d[2 * j], d[2 * j + 1]);
+        if (!(q <= r)) r = q;
+    }
+    return r;
+}
+
+/* x (.) (1 + h delta) in extended range */
+static void xupdate(int n, xc *x, const double *delta, double h)
+{
+    for (int j = 0; j < n; ++j)
+        x[j] = xmul(x[j], xnorm(mk(1.0 + h * delta[2 * j], h * delta[2 * j + 1]), 0));
+}
+
+/*
+ * orc_track with extended-range state (SURVEY O2/O4 for the large-lifting start points): the
+ * same control flow, step control and statuses as orc_track; x = xm 2^xe in/out.
+ */
+int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
+                int64_t p, double *xm, int64_t *xe, double *tau, const double *opt, const int32_t *iopt,
+                uint8_t *status, int64_t *stats)
+{
+    if (n < 1 || n > 64) return -1;
+    orc_sys s = {n, off, a, c, w};
+    const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
+    const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
+    const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < p; ++q) {
+        xc xq[64], xt[64];
+        double dE[128], dN[128];
+        for (int j = 0; j < n; ++j) xq[j] = xnorm(load(xm + 2 * (q * n + j)), xe[q * n + j]);
+        double tq = tau[q], dt = dtau_init;
+        int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
+        int succ = 0, st = 0;
+        if (!isfinite(tq)) {
+            status[q] = ORC_PT_NONFINITE;
+            for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
+            continue;
+        }
+        while (tq < 0.0) {
+            if (steps == max_steps) { st = ORC_PT_MAX_STEPS; break; }
+            double h = fmin(dt, -tq);
+            int s1 = solve_point_x(&s, xq, tq, dE, 0);
+            ++evals;
+            int ok = 0;
+            double tt = tq + h;
+            if (!s1) {
+                double prev = INFINITY;
+                for (int j = 0; j < n; ++j) xt[j] = xq[j];
+                xupdate(n, xt, dE, h);
+                for (int it = 1; it <= K; ++it) {
+                    s1 = solve_point_x(&s, xt, tt, 0, dN);
+                    ++evals;
+                    if (s1) break;
+                    double nd = relmax_d(n, dN);
+                    xupdate(n, xt, dN, 1.0);
+                    if (nd <= newton_tol) { ok = 1; break; }
+                    if (it >= 2 && nd > 0.5 * prev) break;
+                    prev = nd;
+                }
+            }
+            if (ok) {
+                for (int j = 0; j < n; ++j) xq[j] = xt[j];
+                tq = tt;
+                ++steps;
+                if (++succ == grow_after) { dt = fmin(grow * dt, dtau_max); succ = 0; }
+            } else {
+                ++rejects;
+                dt *= shrink;
+                succ = 0;
+                if (dt < dtau_min) { st = (s1 & ORC_PT_SINGULAR) ? ORC_PT_SINGULAR : ORC_PT_STEP_UNDERFLOW; break; }
+            }
+        }
+        if (st == 0) {
+            int conv = 0;
+            for (int it = 1; it <= final_iters; ++it) {
+                int s1 = solve_point_x(&s, xq, 0.0, 0, dN);
+                ++evals; ++fin;
+                if (s1) break;
+                double nd = relmax_d(n, dN);
+                xupdate(n, xq, dN, 1.0);
+                if (nd <= final_tol) { conv = 1; break; }
+            }
+            double lmax = -INFINITY;
+            for (int j = 0; j < n; ++j) lmax = fmax(lmax, xabs_log2(xq[j]));
+            st = (conv && lmax <= log2(inf_norm)) ? ORC_PT_OK : ORC_PT_DIVERGED;
+        }
+        for (int j = 0; j < n; ++j) { store(xm + 2 * (q * n + j), xq[j].m); xe[q * n + j] = xq[j].e; }
         tau[q] = tq;
         status[q] = (uint8_t)st;
         stats[4 * q + 0] = steps;

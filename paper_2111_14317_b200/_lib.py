@@ -45,7 +45,8 @@ class TrackOpts(ctypes.Structure):
     _fields_ = [("dtau_init", ctypes.c_double), ("dtau_min", ctypes.c_double), ("dtau_max", ctypes.c_double),
                 ("newton_tol", ctypes.c_double), ("shrink", ctypes.c_double), ("grow", ctypes.c_double),
                 ("final_tol", ctypes.c_double), ("inf_norm", ctypes.c_double), ("newton_iters", ctypes.c_int32),
-                ("grow_after", ctypes.c_int32), ("max_steps", ctypes.c_int32), ("final_iters", ctypes.c_int32)]
+                ("grow_after", ctypes.c_int32), ("max_steps", ctypes.c_int32), ("final_iters", ctypes.c_int32),
+                ("log_state", ctypes.c_int32)]
 
 
 class PhtError(RuntimeError):

@@ -65,6 +65,7 @@ struct Args {
 struct TrackOpts {
     double dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm;
     int K, grow_after, max_steps, final_iters;
+    int log_state; // state arrays hold z = log x instead of x
 };
 struct TrackArgs {
     int64_t P;
@@ -317,6 +318,7 @@ struct RowAcc {
         eh = e * LN2_HI;
         el = e * LN2_LO;
     }
+    __device__ __forceinline__ double reduced(double phi) const { return (phi - eh) - el; }
     __device__ __forceinline__ double reduce(double phi)
     {
         double y = (phi - eh) - el;
@@ -375,9 +377,11 @@ __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int
         double pa, pb, ta, tb;
         phi_theta<N>(a, pl, tau, pa, ta);
         phi_theta<N>(b, pl, tau, pb, tb);
-        const double ya = acc.reduce(pa);
+        // both rescale checks first: a rescale triggered by b must also apply to a's term
+        acc.reduce(pa);
+        acc.reduce(pb);
+        const double ya = acc.reduced(pa), yb = acc.reduced(pb);
         const double2 wa = expcis(ya, ta, sm.exptab, sm.cistab);
-        const double yb = acc.reduce(pb);
         const double2 wb = expcis(yb, tb, sm.exptab, sm.cistab);
         acc.add(a, wa);
         acc.add(b, wb);
@@ -759,7 +763,23 @@ __device__ __forceinline__ void trk_finish(TrackSmem<N> &T, const TrackArgs &A, 
     T.done_path[q] = pth;
 }
 
-template <int N>
+// z <- z + log(1 + u): the affine update x <- x (1 + u) in logarithmic coordinates
+__device__ __forceinline__ double2 zlog1p_add(double2 z, double2 u)
+{
+    const double re = 0.5 * log1p(fma(u.x, 2.0 + u.x, u.y * u.y));
+    const double im = atan2(u.y, 1.0 + u.x);
+    return make_double2(z.x + re, z.y + im);
+}
+
+template <int N, bool LOGS>
+__device__ __forceinline__ double2 trk_update(double2 v, double2 delta, double h)
+{
+    if (LOGS) return zlog1p_add(v, make_double2(h * delta.x, h * delta.y));
+    const double2 d = cmul(v, delta);
+    return make_double2(fma(h, d.x, v.x), fma(h, d.y, v.y));
+}
+
+template <int N, bool LOGS>
 __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys S, const TrackArgs A)
 {
     using G = Geo<N>;
@@ -790,7 +810,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
             if (T.refill[qq]) T.xa[j][qq] = A.x[T.path[qq] * N + j];
             const int ph = T.phase[qq];
-            sm.xs[j][qq] = (ph == PH_CORRECT) ? T.xt[j][qq] : (ph == PH_IDLE ? make_double2(1.0, 0.0) : T.xa[j][qq]);
+            sm.xs[j][qq] = (ph == PH_CORRECT) ? T.xt[j][qq]
+                                              : (ph == PH_IDLE ? make_double2(LOGS ? 0.0 : 1.0, 0.0) : T.xa[j][qq]);
         }
         __syncthreads();
         if (tid < WL) {
@@ -801,12 +822,12 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             const int ph = (tid < PTS) ? T.phase[tid] : PH_IDLE;
             sm.tau[tid] = (ph == PH_CORRECT) ? T.tau_t[tid] : ((ph == PH_PREDICT) ? T.tau_a[tid] : 0.0);
             if (tid >= PTS)
-                for (int j = 0; j < N; ++j) sm.xs[j][tid] = make_double2(1.0, 0.0);
+                for (int j = 0; j < N; ++j) sm.xs[j][tid] = make_double2(LOGS ? 0.0 : 1.0, 0.0);
         }
         if (tid == 0) T.active = 0;
         __syncthreads();
-        // (2) evaluation + solve at the query points (same code as pht_pc_step)
-        stage1<N, MODE_STEP>(sm, tid);
+        // (2) evaluation + solve at the query points (same code as pht_pc_step / evaluate_log)
+        stage1<N, LOGS ? MODE_EVAL_Z : MODE_STEP>(sm, tid);
         if (tid < WL && tid >= PTS)
             for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
         __syncthreads();
@@ -833,17 +854,15 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             const int qq = tid / N, j = tid % N;
             const int ph = T.phase[qq];
             if (sm.st[qq] == 0 && ph != PH_IDLE) {
+                const double2 dl = T.dd[j][qq];
                 if (ph == PH_PREDICT) {
                     const double h = fmin(T.dt[qq], -T.tau_a[qq]);
-                    const double2 xv = T.xa[j][qq], d = cmul(xv, T.dd[j][qq]);
-                    T.xt[j][qq] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
+                    T.xt[j][qq] = trk_update<N, LOGS>(T.xa[j][qq], dl, h);
                 } else if (ph == PH_CORRECT) {
-                    const double2 xv = T.xt[j][qq], dl = T.dd[j][qq], d = cmul(xv, dl);
-                    T.xt[j][qq] = make_double2(xv.x + d.x, xv.y + d.y);
+                    T.xt[j][qq] = trk_update<N, LOGS>(T.xt[j][qq], dl, 1.0);
                     T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_j / x_j|^2 (reading R14)
                 } else { // FINAL
-                    const double2 xv = T.xa[j][qq], dl = T.dd[j][qq], d = cmul(xv, dl);
-                    T.xa[j][qq] = make_double2(xv.x + d.x, xv.y + d.y);
+                    T.xa[j][qq] = trk_update<N, LOGS>(T.xa[j][qq], dl, 1.0);
                     T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y);
                 }
             }
@@ -889,13 +908,14 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 T.fin[qq] += 1;
                 if (bad) finish = 32;
                 else {
-                    double nd = 0.0, xinf = 0.0;
+                    double nd = 0.0, xinf = 0.0; // xinf: max |x_j| (or max Re z_j in log state)
                     for (int j = 0; j < N; ++j) {
                         nd = fmax(nd, T.nd2[j][qq]);
                         const double2 v = T.xa[j][qq];
-                        xinf = fmax(xinf, sqrt(fma(v.x, v.x, v.y * v.y)));
+                        xinf = fmax(xinf, LOGS ? v.x : sqrt(fma(v.x, v.x, v.y * v.y)));
                     }
-                    if (sqrt(nd) <= o.final_tol) finish = (xinf <= o.inf_norm) ? 0 : 32;
+                    const bool finite = LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm);
+                    if (sqrt(nd) <= o.final_tol) finish = finite ? 0 : 32;
                     else if (T.fin[qq] >= o.final_iters) finish = 32;
                 }
             }
@@ -927,8 +947,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
     }
 }
 
-template <int N>
-cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+template <int N, bool LOGS>
+cudaError_t launch_track_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
     const size_t sb = sizeof(TrackSmem<N>);
     static std::atomic<unsigned long long> configured{0};
@@ -936,19 +956,25 @@ cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t strea
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(configured.load() & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_track<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        cudaError_t e = cudaFuncSetAttribute(k_track<N, LOGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
         if (e != cudaSuccess) return e;
         configured.fetch_or(bit);
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track<N>, Geo<N>::NT, sb);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_track<N, LOGS>, Geo<N>::NT, sb);
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)sms * per_sm;
     const int64_t need = (A.P + Geo<N>::PTS - 1) / Geo<N>::PTS;
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    k_track<N><<<dim3((unsigned)grid), dim3(Geo<N>::NT), sb, stream>>>(S, A);
+    k_track<N, LOGS><<<dim3((unsigned)grid), dim3(Geo<N>::NT), sb, stream>>>(S, A);
     return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+{
+    return A.o.log_state ? launch_track_t<N, true>(S, A, stream, sms) : launch_track_t<N, false>(S, A, stream, sms);
 }
 
 template <int N, int MODE>

@@ -228,3 +228,29 @@ def test_pc_step_host_equals_device(P):
     xh, th = x.copy(), tau.copy()
     g.pc_step_host(xh, th, dtau)
     assert np.array_equal(xh, xd.cpu().numpy()) and np.array_equal(th, td.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,n", [("cyclic-5", 5), ("noon-5", 5), ("cyclic-10", 10)])
+def test_evaluate_log_extreme_rows(P, name, n):
+    """Rows whose terms span more than e^512 (online rescale mid-row), including the case where
+    the second term of a processed pair triggers the rescale: GPU vs extended-range oracle."""
+    sysm = {"cyclic-5": W.cyclic(5, lift_max=100), "noon-5": W.noon(5, lift_max=1000),
+            "cyclic-10": W.cyclic(10, lift_max=100)}[name]
+    z, tau = W.random_log_points(200, n, seed=17, rho_max=300.0, tau_lo=-8.0)
+    g = P.System.from_workload(sysm)
+    Hl, Jz, Jtau, e2, st = g.evaluate_log(_cuda(z), _cuda(tau))
+    e = np.floor(z.real / np.log(2)).astype(np.int64)
+    xm = np.exp(z.real - e * np.log(2)) * np.exp(1j * z.imag)
+    te = np.floor(tau / np.log(2)).astype(np.int64)
+    tm = np.exp(tau - te * np.log(2))
+    o = oracle.Oracle(sysm).evaluate_x(xm, e, tm, te)
+    H, e2 = Hl.cpu().numpy(), e2.cpu().numpy().astype(np.int64)
+    worst = 0.0
+    for q in range(len(z)):
+        for k in range(n):
+            ls = o["LSH"][q, k]
+            ref = o["Hm"][q, k] * np.exp2(float(o["He"][q, k] - ls))
+            got = H[q, k] * np.exp2(float(e2[q, k] - ls))
+            worst = max(worst, abs(got - ref))
+    # a-priori bound (reading R9/A27): ~2.7 u * max|phi| ~ 1e-12 here
+    assert worst <= 1e-10, worst

@@ -97,3 +97,39 @@ def test_track_many_slots_queue(P):
     assert np.all(sg == 0)
     ref = xg[:4]
     assert np.array_equal(xg, np.tile(ref, (5000, 1)))
+
+
+def _log_state_parity(P, sysm, z, tau0):
+    g = P.System.from_workload(sysm)
+    zd, td = _cuda(z), _cuda(tau0)
+    st, stats = g.track(zd, td, log_state=1)
+    zg, sg, stg = zd.cpu().numpy(), st.cpu().numpy(), stats.cpu().numpy()
+    m, e = oracle.z_to_x(z)
+    xm, xe, to, so, sto = oracle.Oracle(sysm).track_x(m, e, tau0)
+    xo = xm * np.exp2(xe.astype(float))
+    xg = np.exp(zg)
+    return xg, sg, stg, xo, so, sto
+
+
+def test_track_log_state_cyclic5_uncapped(P):
+    """log-coordinate state (opts.log_state) from the full-range start points vs orc_track_x."""
+    c5 = W.cyclic(5, lift_max=100)
+    _, tau0, _, z = SS.start_points(c5)
+    xg, sg, stg, xo, so, sto = _log_state_parity(P, c5, z, tau0)
+    assert np.sum(sg == 0) == np.sum(so == 0) == 70
+    rel = np.linalg.norm(xg - xo, axis=1) / np.linalg.norm(xo, axis=1)
+    assert rel.max() <= 1e-8, rel.max()
+    assert len({tuple(np.round(v, 7)) for v in xg}) == 70
+
+
+def test_track_log_state_noon5(P):
+    """noon-5 (233 paths = 3^5 - 10) from LP-enumerated cells, |Re z| in the thousands."""
+    s = W.noon(5, lift_max=1000)
+    _, tau0, _, z = SS.start_points(s, fast=True)
+    assert len(z) == 233
+    xg, sg, stg, xo, so, sto = _log_state_parity(P, s, z, tau0)
+    assert np.sum(sg == 0) == np.sum(so == 0)
+    both = (sg == 0) & (so == 0)
+    rel = np.linalg.norm(xg[both] - xo[both], axis=1) / np.linalg.norm(xo[both], axis=1)
+    assert rel.max() <= 1e-8, rel.max()
+    assert np.sum(sg == 0) >= 0.9 * 233

@@ -91,3 +91,33 @@ def test_known_mixed_volumes():
     assert sum(c["volume"] for c in SS.mixed_cells_fast(W.noon(4, lift_max=1000))) == 3 ** 4 - 8
     assert sum(c["volume"] for c in SS.mixed_cells_fast(W.noon(5, lift_max=1000))) == 3 ** 5 - 10
     assert sum(c["volume"] for c in SS.mixed_cells_fast(W.cyclic(7, lift_max=10 ** 4))) == 924
+
+
+def test_extended_range_tracker_matches_double_tracker_in_range():
+    """orc_track_x (extended range) follows the same algorithm as orc_track: same endpoints when
+    the data fit in double (the only difference is the representation)."""
+    c5 = W.cyclic(5, lift_max=100)
+    x, tau0, _, z = SS.start_points(c5, zmax=20)
+    o = oracle.Oracle(c5)
+    xa, ta, sa, _ = o.track(x, tau0)
+    m, e = oracle.z_to_x(z)
+    xm, xe, tb, sb, _ = o.track_x(m, e, tau0)
+    xb = xm * np.exp2(xe.astype(float))
+    assert np.array_equal(sa, sb)
+    assert np.max(np.abs(xa - xb) / np.abs(xa)) < 1e-10
+
+
+def test_extended_range_tracker_uncapped_start_points():
+    """Start points at the full tau0 = -37/gap (|Re z| up to ~350, outside double range for the
+    monomials) -> 70 distinct finite solutions of cyclic-5."""
+    c5 = W.cyclic(5, lift_max=100)
+    _, tau0, _, z = SS.start_points(c5)
+    assert np.abs(z.real).max() > 300
+    o = oracle.Oracle(c5)
+    m, e = oracle.z_to_x(z)
+    xm, xe, te, st, _ = o.track_x(m, e, tau0)
+    assert np.all(st == 0)
+    xend = xm * np.exp2(xe.astype(float))
+    r = o.evaluate(xend, np.ones(70))
+    assert np.max(np.abs(r["H"]) / r["SH"]) < 1e-13
+    assert len({tuple(np.round(v, 7)) for v in xend}) == 70

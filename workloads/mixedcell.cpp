@@ -273,34 +273,39 @@ extern "C" int64_t mc_cells(int n, const int64_t *off, const int32_t *exps, cons
         }
     }
     sv.lower_edges();
-    // search order: supports with fewer lower edges first
-    std::vector<int> order(n);
-    for (int k = 0; k < n; ++k) order[k] = k;
-    std::sort(order.begin(), order.end(), [&](int x, int y) { return sv.edges[x].size() < sv.edges[y].size(); });
-    // pairwise compatibility table
-    std::vector<std::vector<std::vector<char>>> comp(n * n);
+    // pairwise compatibility as bitsets: comp[x][y][i] = edges of y compatible with edge i of x
+    std::vector<int> nw(n);
+    for (int y = 0; y < n; ++y) nw[y] = ((int)sv.edges[y].size() + 63) / 64;
+    std::vector<std::vector<std::vector<std::vector<uint64_t>>>> comp(n, std::vector<std::vector<std::vector<uint64_t>>>(n));
     for (int x = 0; x < n; ++x)
-        for (int y = x + 1; y < n; ++y) {
-            auto &tab = comp[x * n + y];
-            tab.assign(sv.edges[x].size(), std::vector<char>(sv.edges[y].size(), 0));
+        for (int y = 0; y < n; ++y) {
+            if (x == y) continue;
+            comp[x][y].assign(sv.edges[x].size(), std::vector<uint64_t>(nw[y], 0));
+        }
+    for (int x = 0; x < n; ++x)
+        for (int y = x + 1; y < n; ++y)
             for (size_t i = 0; i < sv.edges[x].size(); ++i)
                 for (size_t j = 0; j < sv.edges[y].size(); ++j) {
                     std::vector<std::pair<int, Edge>> ch{{x, sv.edges[x][i]}, {y, sv.edges[y][j]}};
-                    tab[i][j] = sv.margin(ch) > 1e-9;
+                    if (sv.margin(ch) > 1e-9) {
+                        comp[x][y][i][j / 64] |= 1ull << (j % 64);
+                        comp[y][x][j][i / 64] |= 1ull << (i % 64);
+                    }
                 }
-        }
-    auto compatible = [&](int x, int i, int y, int j) -> bool {
-        if (x < y) return comp[x * n + y][i][j];
-        return comp[y * n + x][j][i];
-    };
     int64_t ncell = 0;
     bool overflow = false;
     std::vector<std::pair<int, Edge>> chosen;
-    std::vector<int> chosen_idx;
-    // iterative DFS via recursion lambda
+    std::vector<char> used(n, 0);
     std::vector<double> alpha;
-    auto dfs = [&](auto &&self, int level) -> void {
+    auto popcnt = [](const std::vector<uint64_t> &b) {
+        int c = 0;
+        for (uint64_t w : b) c += __builtin_popcountll(w);
+        return c;
+    };
+    // cand[y]: edges of support y compatible (pairwise) with every chosen edge
+    auto dfs = [&](auto &&self, std::vector<std::vector<uint64_t>> &cand) -> void {
         if (overflow) return;
+        const int level = (int)chosen.size();
         if (level == n) {
             double t = sv.margin(chosen, &alpha);
             if (!(t > 1e-9)) return;
@@ -311,7 +316,6 @@ extern "C" int64_t mc_cells(int n, const int64_t *off, const int32_t *exps, cons
                 pairs_out[(ncell * n + k) * 2 + 1] = sv.S[k].gid[ce.second.q];
             }
             for (int j = 0; j < n; ++j) alpha_out[ncell * n + j] = alpha[j];
-            // gap: smallest slack over all supports (every support is involved at a leaf)
             double gap = INFINITY;
             for (auto &ce : chosen) {
                 const Support &s = sv.S[ce.first];
@@ -329,20 +333,43 @@ extern "C" int64_t mc_cells(int n, const int64_t *off, const int32_t *exps, cons
             ++ncell;
             return;
         }
-        const int k = order[level];
-        for (int e = 0; e < (int)sv.edges[k].size(); ++e) {
-            bool ok = true;
-            for (int l = 0; l < level && ok; ++l) ok = compatible(order[l], chosen_idx[l], k, e);
-            if (!ok) continue;
-            chosen.push_back({k, sv.edges[k][e]});
-            chosen_idx.push_back(e);
-            ++sv.nodes;
-            if (level + 1 == n || level < 1 || sv.margin(chosen) > 1e-9) self(self, level + 1);
-            chosen.pop_back();
-            chosen_idx.pop_back();
+        // dynamic ordering: the unused support with the fewest candidates (forward checking)
+        int k = -1, best = 1 << 30;
+        for (int y = 0; y < n; ++y) {
+            if (used[y]) continue;
+            int c = popcnt(cand[y]);
+            if (c == 0) return;
+            if (c < best) { best = c; k = y; }
         }
+        used[k] = 1;
+        for (int e = 0; e < (int)sv.edges[k].size(); ++e) {
+            if (!((cand[k][e / 64] >> (e % 64)) & 1)) continue;
+            chosen.push_back({k, sv.edges[k][e]});
+            ++sv.nodes;
+            if (level + 1 == n || level < 1 || sv.margin(chosen) > 1e-9) {
+                std::vector<std::vector<uint64_t>> next(cand);
+                bool dead = false;
+                for (int y = 0; y < n && !dead; ++y) {
+                    if (used[y]) continue;
+                    int c = 0;
+                    for (int w = 0; w < nw[y]; ++w) {
+                        next[y][w] &= comp[k][y][e][w];
+                        c += __builtin_popcountll(next[y][w]);
+                    }
+                    dead = (c == 0);
+                }
+                if (!dead) self(self, next);
+            }
+            chosen.pop_back();
+        }
+        used[k] = 0;
     };
-    dfs(dfs, 0);
+    std::vector<std::vector<uint64_t>> cand0(n);
+    for (int y = 0; y < n; ++y) {
+        cand0[y].assign(nw[y], 0);
+        for (int e = 0; e < (int)sv.edges[y].size(); ++e) cand0[y][e / 64] |= 1ull << (e % 64);
+    }
+    dfs(dfs, cand0);
     if (stats) {
         stats[0] = sv.lps;
         stats[1] = sv.nodes;

@@ -22,6 +22,10 @@ from typing import List, Tuple
 
 import numpy as np
 
+import os
+
+DATA_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
+
 
 def _solve_rational(V: List[List[int]], b: List[Fraction]):
     """Gaussian elimination over Q; returns x or None if singular."""
@@ -228,3 +232,31 @@ def start_points(system, L: float = 37.0, tau_cap: float | None = None, zmax: fl
         taus.append(np.full(len(x), t0))
         ids.append(np.full(len(x), ci))
     return (np.concatenate(xs), np.concatenate(taus), np.concatenate(ids), np.concatenate(zs))
+
+
+def load_cells(name: str, lift_max: int):
+    """Cells stored by workloads.make_starts (exact rational alpha/gap restored)."""
+    d = np.load(os.path.join(DATA_DIR, f"{name}_L{lift_max}.npz"), allow_pickle=False)
+    cells = []
+    for c in range(len(d["volume"])):
+        pr = [(int(a), int(b)) for a, b in d["pairs"][c]]
+        al = [Fraction(int(nu), int(de)) for nu, de in zip(d["alpha_num"][c], d["alpha_den"][c])]
+        cells.append({"pairs": pr, "alpha": al, "gap": Fraction(d["gap"][c]).limit_denominator(10**12),
+                      "volume": int(d["volume"][c]), "V": None})
+    return cells
+
+
+def start_points_from_cells(system, cells, L: float = 37.0):
+    """Start points (log coordinates z, tau0 per path, cell ids) from stored cells."""
+    n = system.n
+    zs, taus, ids = [], [], []
+    for ci, cell in enumerate(cells):
+        if cell.get("V") is None:
+            cell = dict(cell)
+            cell["V"] = [[int(system.exps[p][j]) - int(system.exps[q][j]) for j in range(n)]
+                         for (p, q) in cell["pairs"]]
+        _, t0, z = cell_start_points(system, cell, L)
+        zs.append(z)
+        taus.append(np.full(len(z), t0))
+        ids.append(np.full(len(z), ci))
+    return np.concatenate(zs), np.concatenate(taus), np.concatenate(ids)
