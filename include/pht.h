@@ -179,6 +179,9 @@ typedef struct {
     int32_t log_state;    /* 0: x holds points x; 1: x holds z = log x (any branch) — for start
                              points far outside double range (|Re z| > ~700); the steps are the
                              same affine updates, applied as z <- z + log(1 + dx/x)            */
+    int32_t pred_log;     /* Euler predictor chart: 0 affine x + h dx/dtau (the paper's form,
+                             P:254-259); 1 log chart z + h dz/dtau (exact for the toric paths
+                             x ~ e^{tau alpha} y near tau0); -1 (default) = log_state          */
 } pht_track_opts;
 
 void pht_track_opts_default(pht_track_opts *opts);

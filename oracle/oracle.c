@@ -580,7 +580,8 @@ static double relmax(int n, const double *d, const double *x)
  * corrector converges when max_j |dN_j|/|x_j| <= newton_tol, a scale-invariant test because
  * polyhedral start points span many orders of magnitude).
  * opt[] = {dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm}
- * iopt[] = {K (max corrector iters), grow_after, max_steps, final_iters}
+ * iopt[] = {K (max corrector iters), grow_after, max_steps, final_iters, pred_log}
+ * pred_log: the Euler predictor in the log chart, x exp(h dz/dtau), instead of x + h dx/dtau.
  * stats[q] = {accepted steps, rejected steps, evaluations (solves), final Newton iters}.
  */
 int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
@@ -592,6 +593,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+    const int pred_log = iopt[4];
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
         double *xq = x + 2 * n * q, dE[128], dN[128], xt[128];
@@ -612,7 +614,15 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             double tt = tq + h;
             if (!s1) {
                 double t = exp(tq), prev = INFINITY;
-                for (int i = 0; i < 2 * n; ++i) xt[i] = xq[i] + h * t * dE[i];
+                if (pred_log) { /* Euler in the log chart: x exp(h dz/dtau), dz/dtau = t dE / x */
+                    for (int j = 0; j < n; ++j) {
+                        cplx xv = load(xq + 2 * j);
+                        cplx dz = cdiv(cmul(mk(t, 0.0), load(dE + 2 * j)), xv);
+                        store(xt + 2 * j, cmul(xv, cexp(h * dz)));
+                    }
+                } else {
+                    for (int i = 0; i < 2 * n; ++i) xt[i] = xq[i] + h * t * dE[i];
+                }
                 for (int it = 1; it <= K; ++it) {
                     s1 = solve_point(&s, xt, exp(tt), 0, dN);
                     ++evals;
@@ -741,6 +751,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+    const int pred_log = iopt[4];
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
         xc xq[64], xt[64];
@@ -764,7 +775,10 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
             if (!s1) {
                 double prev = INFINITY;
                 for (int j = 0; j < n; ++j) xt[j] = xq[j];
-                xupdate(n, xt, dE, h);
+                if (pred_log) /* Euler in the log chart: x exp(h delta_E) */
+                    for (int j = 0; j < n; ++j) xt[j] = xmul(xt[j], xnorm(cexp(h * load(dE + 2 * j)), 0));
+                else
+                    xupdate(n, xt, dE, h);
                 for (int it = 1; it <= K; ++it) {
                     s1 = solve_point_x(&s, xt, tt, 0, dN);
                     ++evals;

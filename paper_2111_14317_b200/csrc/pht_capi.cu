@@ -307,6 +307,7 @@ extern "C" void pht_track_opts_default(pht_track_opts *o)
     o->max_steps = 10000;
     o->final_iters = 5;
     o->log_state = 0;
+    o->pred_log = -1;
 }
 
 extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau, const pht_track_opts *opts,
@@ -336,7 +337,8 @@ extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau,
     A.stats = (long long *)stats;
     A.queue = ctr;
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
-                         o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state};
+                         o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
+                         o.pred_log < 0 ? o.log_state : o.pred_log};
     switch (s->n) {
 #define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)

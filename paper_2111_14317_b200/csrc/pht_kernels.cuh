@@ -66,6 +66,7 @@ struct TrackOpts {
     double dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm;
     int K, grow_after, max_steps, final_iters;
     int log_state; // state arrays hold z = log x instead of x
+    int pred_log;  // Euler predictor in the log chart: z + h dz/dtau (x exp(h dz/dtau))
 };
 struct TrackArgs {
     int64_t P;
@@ -771,6 +772,17 @@ __device__ __forceinline__ double2 zlog1p_add(double2 z, double2 u)
     return make_double2(z.x + re, z.y + im);
 }
 
+// Euler predictor in the log chart: z + h delta (log state) or x exp(h delta) (x state)
+template <bool LOGS>
+__device__ __forceinline__ double2 trk_predict_log(double2 v, double2 delta, double h)
+{
+    if (LOGS) return make_double2(fma(h, delta.x, v.x), fma(h, delta.y, v.y));
+    double sn, cs;
+    sincos(h * delta.y, &sn, &cs);
+    const double m = exp(h * delta.x);
+    return cmul(v, make_double2(m * cs, m * sn));
+}
+
 template <int N, bool LOGS>
 __device__ __forceinline__ double2 trk_update(double2 v, double2 delta, double h)
 {
@@ -857,7 +869,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 const double2 dl = T.dd[j][qq];
                 if (ph == PH_PREDICT) {
                     const double h = fmin(T.dt[qq], -T.tau_a[qq]);
-                    T.xt[j][qq] = trk_update<N, LOGS>(T.xa[j][qq], dl, h);
+                    T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], dl, h)
+                                             : trk_update<N, LOGS>(T.xa[j][qq], dl, h);
                 } else if (ph == PH_CORRECT) {
                     T.xt[j][qq] = trk_update<N, LOGS>(T.xt[j][qq], dl, 1.0);
                     T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_j / x_j|^2 (reading R14)

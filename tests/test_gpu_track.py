@@ -132,4 +132,4 @@ def test_track_log_state_noon5(P):
     both = (sg == 0) & (so == 0)
     rel = np.linalg.norm(xg[both] - xo[both], axis=1) / np.linalg.norm(xo[both], axis=1)
     assert rel.max() <= 1e-8, rel.max()
-    assert np.sum(sg == 0) >= 0.9 * 233
+    assert np.sum(sg == 0) == 233

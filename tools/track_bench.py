@@ -15,6 +15,7 @@ from workloads import startsys as SS  # noqa: E402
 from workloads.make_starts import CONFIGS  # noqa: E402
 
 res = {}
+OPTS = json.loads(os.environ.get("TB_OPTS", "{}"))
 which = sys.argv[1:] or ["katsura-10:10000", "noon-10:10000", "cyclic-10:1000000"]
 for item in which:
     name, L = item.split(":")
@@ -31,7 +32,7 @@ for item in which:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st, stats = g.track(zd, td, log_state=1)
+        st, stats = g.track(zd, td, log_state=1, **OPTS)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -41,5 +42,6 @@ for item in which:
                steps_mean=float(stats[:, 0].mean()), steps_max=int(stats[:, 0].max()), evals_total=int(stats[:, 2].sum()),
                evals_per_s=float(stats[:, 2].sum() / ms * 1e3), start_prep_s=prep,
                max_abs_re_z0=float(np.abs(z.real).max()), tau0_min=float(tau0.min()))
+    out["opts"] = OPTS
     res[f"{name}:L{L}"] = out
     print(json.dumps({f"{name}:L{L}": out}), flush=True)
