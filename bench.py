@@ -180,6 +180,68 @@ def cpu_baseline(seconds_target=15.0):
                       f"{dt:.1f} s on {cores} threads"}
 
 
+TRACK_CONFIGS = [("katsura-10", 10_000, "BASELINE.json configs[1]: katsura-10 full path tracking"),
+                 ("noon-10", 10_000, "BASELINE.json configs[4]: noon-10 (large liftings) tracked to t=1 + endpoint gather"),
+                 ("cyclic-10", 1_000_000, "BASELINE.json configs[2]: cyclic-10 predictor-corrector tracking, sharded")]
+
+
+def tracking_section(world, rank, dev, which):
+    """Full path tracking of the stored start systems (log-coordinate state, device tracker).
+    Each rank tracks its shard; ONE gather of endpoints/status/stats to rank 0 is inside the
+    timed region (SURVEY §8(d) 'paths/sec' clock; §8(e) single collective)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2111_14317_b200 as P
+    from paper_2111_14317_b200.shard import gather_to_rank0, shard_indices
+    from workloads import startsys as SS
+    from workloads.make_starts import CONFIGS
+    out = {}
+    for name, L, label in TRACK_CONFIGS:
+        if which and name not in which:
+            continue
+        sysm = CONFIGS[name](L)
+        cells = SS.load_cells(name, L)
+        w0, tau0, cid = SS.start_points_cells(sysm, cells)   # cell coordinates (pht_track_cells)
+        wcell = torch.from_numpy(SS.cell_lifts_fast(sysm, cells)).to(dev)
+        Ptot = len(w0)
+        idx = shard_indices(Ptot, rank, world, seed=17)
+        g = P.System.from_workload(sysm, device=dev.index)
+        zl = torch.from_numpy(np.ascontiguousarray(w0[idx])).to(dev)
+        tl = torch.from_numpy(np.ascontiguousarray(tau0[idx])).to(dev)
+        cl = torch.from_numpy(np.ascontiguousarray(cid[idx])).to(dev)
+        # warm-up on a copy (first launch configures the kernel)
+        g.track_cells(zl[:64].clone(), tl[:64].clone(), wcell, cl[:64].clone())
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st, stats = g.track_cells(zl, tl, wcell, cl)
+        if world > 1:
+            res = gather_to_rank0({"z": zl, "status": st, "stats": stats}, idx, Ptot)
+        else:
+            res = {"z": zl, "status": st, "stats": stats}
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            stv = res["status"].cpu().numpy()
+            sts = res["stats"].cpu().numpy()
+            names = {0: "finite", 2: "nonfinite", 4: "singular", 8: "step_underflow", 16: "max_steps",
+                     32: "diverged"}
+            hist = {names.get(int(k), str(int(k))): int(v) for k, v in zip(*np.unique(stv, return_counts=True))}
+            t = float(ms.item())
+            out[name] = {"workload": label, "paths": Ptot, "mixed_volume": int(sum(c["volume"] for c in cells)),
+                         "lift_max": L, "ms": t, "paths_per_s": Ptot / (t * 1e-3), "status": hist,
+                         "steps_mean": float(sts[:, 0].mean()), "steps_max": int(sts[:, 0].max()),
+                         "evals": int(sts[:, 2].sum()), "evals_per_s": float(sts[:, 2].sum() / (t * 1e-3)),
+                         "state": "cell coordinates (pht_track_cells), log-chart Euler predictor, default opts"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -190,6 +252,8 @@ def main():
     ap.add_argument("--ref-points", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--tracking", default="katsura-10,noon-10,cyclic-10",
+                    help="comma list of tracked configs ('' to skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -263,6 +327,9 @@ def main():
         dist.all_reduce(te_ms, op=dist.ReduceOp.MAX)
     e2e_value = 2.0 * Pn * world * args.e2e_steps / (float(te_ms.item()) * 1e-3)
 
+    tracking = tracking_section(world, rank, dev, [t for t in args.tracking.split(",") if t]) \
+        if args.tracking else {}
+
     if rank == 0:
         clocks = clk.summary() or {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
         fl = algorithmic_flops_per_eval(sysm)
@@ -288,6 +355,7 @@ def main():
                     "d2h_bytes_per_step": Pn * (16 * N_VARS + 8 + 1 + 8)},
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "tracking": tracking,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()

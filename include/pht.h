@@ -189,6 +189,24 @@ void pht_track_opts_default(pht_track_opts *opts);
 int pht_track(const pht_system *sys, int64_t p, double *x, double *tau, const pht_track_opts *opts,
               int64_t *stats, uint8_t *status, void *stream);
 
+/*
+ * Tracking in cell coordinates ("rescaled" polyhedral homotopy).  For a start path of the mixed
+ * cell with inner normal (alpha, 1) and lower values beta_k, the substitution x = e^{tau alpha} e^w
+ * and row scaling by e^{-tau beta_k} turn Eq. (2) into the polyhedral homotopy
+ *     h'_k(w, tau) = sum_i c_i e^{<a_i, w>} e^{tau omega'_i},  omega'_i = omega_i + <a_i, alpha> - beta_k,
+ * whose start values w = log y are O(1) and which equals F(e^w) at tau = 0 (so w = log x there).
+ * It is the same path, with no cancellation between huge <a, log x> and omega tau.
+ *   w          c128[p][n] start values w0 = log y (log state; opts->log_state is implied), out: z = log x.
+ *   tau        double[p] tau0 in, 0 out.
+ *   cell_lift  DEVICE double[ncells][M] shifted liftings omega' of every term (M = packed term count
+ *              = input term count; systems with zero coefficients are rejected, PHT_EINVAL).
+ *   path_cell  DEVICE int32[p] cell of each path (out-of-range ids give status PHT_PT_NONFINITE).
+ * Other arguments as pht_track.
+ */
+int pht_track_cells(const pht_system *sys, int64_t p, double *w, double *tau, const double *cell_lift,
+                    int64_t ncells, const int32_t *path_cell, const pht_track_opts *opts,
+                    int64_t *stats, uint8_t *status, void *stream);
+
 /* Number of kernels this library has launched in the calling process (all handles). */
 int64_t pht_launch_count(void);
 

@@ -152,8 +152,9 @@ class Oracle:
 
     def track_x(self, xm, xe, tau, *, dtau_init=0.05, dtau_min=1e-8, dtau_max=0.5, newton_tol=1e-10,
                 shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
-                max_steps=10000, final_iters=5, pred_log=1):
-        """orc_track_x: the tracker with extended-range state x = xm * 2**xe."""
+                max_steps=10000, final_iters=5, pred_log=1, cell_lift=None, path_cell=None):
+        """orc_track_x: the tracker with extended-range state x = xm * 2**xe; with cell_lift
+        [ncells, M] / path_cell [p] it tracks in cell coordinates (pht_track_cells)."""
         xm = _c2(xm).copy()
         xe = np.ascontiguousarray(xe, np.int64).copy()
         tau = np.ascontiguousarray(tau, np.float64).copy()
@@ -162,8 +163,11 @@ class Oracle:
         iopt = np.array([K, grow_after, max_steps, final_iters, pred_log], np.int32)
         st = np.zeros(p, np.uint8)
         stats = np.zeros((p, 4), np.int64)
+        cw = None if cell_lift is None else np.ascontiguousarray(cell_lift, np.float64)
+        pc = None if path_cell is None else np.ascontiguousarray(path_cell, np.int32)
         rc = lib().orc_track_x(*self._sys_args(), ctypes.c_int64(p), _p(xm), _p(xe), _p(tau), _p(opt),
-                               _p(iopt), _p(st), _p(stats))
+                               _p(iopt), _p(st), _p(stats), _p(cw) if cw is not None else None,
+                               _p(pc) if pc is not None else None)
         assert rc == 0
         return xm, xe, tau, st, stats
 

@@ -268,8 +268,12 @@ static double xabs_log2(xc a) /* log2 |a|, for the scale sums */
  * Extended-range evaluation of one point (the same definition as eval_point):
  * x[j], t as xc values; outputs H[k], Jx[k*n+j], Jt[k] and the absolute term sums (xc).
  */
-static void eval_point_x(const orc_sys *s, const xc *x, xc t, xc *H, xc *Jx, xc *Jt,
-                         xc *SH, xc *SJx, xc *SJt)
+static xc xexp_real(double tau);
+
+/* wr (optional): real per-term liftings omega' (cell-shifted, pht_track_cells); then the t-powers
+ * are e^{tau omega'} (Eq. (2)) and Jt receives dh/dtau = sum omega' T instead of dh/dt. */
+static void eval_point_x_w(const orc_sys *s, const xc *x, xc t, double tau, const double *wr, xc *H, xc *Jx,
+                           xc *Jt, xc *SH, xc *SJx, xc *SJt)
 {
     const int n = s->n;
     xc r[64];
@@ -281,7 +285,7 @@ static void eval_point_x(const orc_sys *s, const xc *x, xc t, xc *H, xc *Jx, xc 
         for (int64_t i = s->off[k]; i < s->off[k + 1]; ++i) {
             const int32_t *ai = s->a + i * n;
             xc cc = xnorm(load(s->c + 2 * i), 0);
-            xc tw = xpow_nat(t, s->w[i]);
+            xc tw = wr ? xexp_real(tau * wr[i]) : xpow_nat(t, s->w[i]);
             xc T = cc;
             for (int j = 0; j < n; ++j)
                 if (ai[j] != 0) T = xmul(T, ai[j] > 0 ? xpow_nat(x[j], ai[j]) : xpow_nat(r[j], -ai[j]));
@@ -299,7 +303,11 @@ static void eval_point_x(const orc_sys *s, const xc *x, xc t, xc *H, xc *Jx, xc 
                 hx[j] = xadd(hx[j], D);
                 shx[j] = xadd(shx[j], xnorm(mk(cabs(D.m), 0), D.e));
             }
-            if (s->w[i] >= 1) {
+            if (wr) { /* d/dtau of c x^a e^{tau omega'} = omega' T */
+                xc D = xmul(T, xnorm(mk(wr[i], 0), 0));
+                ht = xadd(ht, D);
+                sht = xadd(sht, xnorm(mk(cabs(D.m), 0), D.e));
+            } else if (s->w[i] >= 1) {
                 xc D = xmul(cc, xnorm(mk((double)s->w[i], 0), 0));
                 for (int j = 0; j < n; ++j)
                     if (ai[j] != 0) D = xmul(D, ai[j] > 0 ? xpow_nat(x[j], ai[j]) : xpow_nat(r[j], -ai[j]));
@@ -317,6 +325,11 @@ static void eval_point_x(const orc_sys *s, const xc *x, xc t, xc *H, xc *Jx, xc 
             if (SJx) SJx[k * n + j] = shx[j];
         }
     }
+}
+
+static void eval_point_x(const orc_sys *s, const xc *x, xc t, xc *H, xc *Jx, xc *Jt, xc *SH, xc *SJx, xc *SJt)
+{
+    eval_point_x_w(s, x, t, 0.0, 0, H, Jx, Jt, SH, SJx, SJt);
 }
 
 /* x_j = xm_j * 2^{xe_j}, t = tm * 2^{te}; outputs as (mantissa, exponent) pairs and the
@@ -683,19 +696,19 @@ static xc xexp_real(double tau)
  * D_z h = Jx diag(x), each row divided by its largest binary exponent (row
  * scaling leaves the solution unchanged), then LU in double:
  * D_z H delta_E = -dH/dtau, D_z H delta_N = -H (dx = x (.) delta). */
-static int solve_point_x(const orc_sys *s, const xc *x, double tau, double *dEr, double *dNr)
+static int solve_point_x(const orc_sys *s, const xc *x, double tau, const double *wr, double *dEr, double *dNr)
 {
     const int n = s->n;
     xc H[64], Jx[64 * 64], Jt[64];
     xc t = xexp_real(tau);
     for (int j = 0; j < n; ++j)
         if (creal(x[j].m) == 0.0 && cimag(x[j].m) == 0.0) return ORC_PT_ZERO_COORD;
-    eval_point_x(s, x, t, H, Jx, Jt, 0, 0, 0);
+    eval_point_x_w(s, x, t, tau, wr, H, Jx, Jt, 0, 0, 0);
     double A[64 * 64 * 2], B[64 * 2 * 2], X[64 * 2 * 2];
     for (int k = 0; k < n; ++k) {
         xc row[66];
         for (int j = 0; j < n; ++j) row[j] = xmul(Jx[k * n + j], x[j]);
-        row[n] = xmul(Jt[k], t);
+        row[n] = wr ? Jt[k] : xmul(Jt[k], t); /* dh/dtau */
         row[n + 1] = H[k];
         int64_t emax = INT64_MIN;
         for (int j = 0; j < n + 2; ++j)
@@ -741,10 +754,12 @@ static void xupdate(int n, xc *x, const double *delta, double h)
 /*
  * orc_track with extended-range state (SURVEY O2/O4 for the large-lifting start points): the
  * same control flow, step control and statuses as orc_track; x = xm 2^xe in/out.
+ * cellw/path_cell (optional): track in cell coordinates with the cell-shifted liftings
+ * omega' = cellw[path_cell[q]][i] (include/pht.h pht_track_cells); t^omega' = e^{tau omega'}.
  */
 int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
                 int64_t p, double *xm, int64_t *xe, double *tau, const double *opt, const int32_t *iopt,
-                uint8_t *status, int64_t *stats)
+                uint8_t *status, int64_t *stats, const double *cellw, const int32_t *path_cell)
 {
     if (n < 1 || n > 64) return -1;
     orc_sys s = {n, off, a, c, w};
@@ -756,6 +771,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
     for (int64_t q = 0; q < p; ++q) {
         xc xq[64], xt[64];
         double dE[128], dN[128];
+        const double *wr = cellw ? cellw + (size_t)path_cell[q] * off[n] : 0;
         for (int j = 0; j < n; ++j) xq[j] = xnorm(load(xm + 2 * (q * n + j)), xe[q * n + j]);
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
@@ -768,7 +784,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
         while (tq < 0.0) {
             if (steps == max_steps) { st = ORC_PT_MAX_STEPS; break; }
             double h = fmin(dt, -tq);
-            int s1 = solve_point_x(&s, xq, tq, dE, 0);
+            int s1 = solve_point_x(&s, xq, tq, wr, dE, 0);
             ++evals;
             int ok = 0;
             double tt = tq + h;
@@ -780,7 +796,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                 else
                     xupdate(n, xt, dE, h);
                 for (int it = 1; it <= K; ++it) {
-                    s1 = solve_point_x(&s, xt, tt, 0, dN);
+                    s1 = solve_point_x(&s, xt, tt, wr, 0, dN);
                     ++evals;
                     if (s1) break;
                     double nd = relmax_d(n, dN);
@@ -805,7 +821,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
         if (st == 0) {
             int conv = 0;
             for (int it = 1; it <= final_iters; ++it) {
-                int s1 = solve_point_x(&s, xq, 0.0, 0, dN);
+                int s1 = solve_point_x(&s, xq, 0.0, wr, 0, dN);
                 ++evals; ++fin;
                 if (s1) break;
                 double nd = relmax_d(n, dN);

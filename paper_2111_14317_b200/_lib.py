@@ -33,6 +33,7 @@ SIGNATURES = {
     "pht_pc_step_host": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "pht_track_opts_default": (None, [ctypes.c_void_p]),
     "pht_track": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pht_track_cells": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pht_launch_count": (_i64, []),
     "pht_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "pht_last_cuda_error": (ctypes.c_char_p, []),

@@ -156,6 +156,31 @@ class System:
                                   _stream(d)), "pht_track")
         return st, sv
 
+    def track_cells(self, w, tau, cell_lift, path_cell, stats: bool = True, **opts):
+        """pht_track_cells: tracking in cell coordinates.  w: complex128 [p, n] start values log y,
+        tau: float64 [p], cell_lift: float64 [ncells, M] cell-shifted liftings, path_cell: int32 [p]
+        (all cuda).  w is replaced by z = log x at tau = 0.  Returns (status, stats)."""
+        self._check_pts(w, tau)
+        p = w.shape[0]
+        d = self._dev()
+        if not (cell_lift.is_cuda and cell_lift.dtype == torch.float64 and cell_lift.dim() == 2
+                and cell_lift.shape[1] == self.M and cell_lift.is_contiguous()):
+            raise PhtError("cell_lift must be a contiguous cuda float64 tensor [ncells, M]")
+        if not (path_cell.is_cuda and path_cell.dtype == torch.int32 and path_cell.shape == (p,)):
+            raise PhtError("path_cell must be a cuda int32 tensor [p]")
+        o = _lib.TrackOpts()
+        self._lib.pht_track_opts_default(ctypes.byref(o))
+        for k, v in opts.items():
+            if not hasattr(o, k):
+                raise PhtError(f"unknown tracker option {k}")
+            setattr(o, k, v)
+        st = torch.empty(p, dtype=torch.uint8, device=d)
+        sv = torch.empty((p, 4), dtype=torch.int64, device=d) if stats else None
+        check(self._lib.pht_track_cells(self._h, p, _ptr(w), _ptr(tau), _ptr(cell_lift), cell_lift.shape[0],
+                                        _ptr(path_cell), ctypes.byref(o), _ptr(sv), _ptr(st), _stream(d)),
+              "pht_track_cells")
+        return st, sv
+
 
 def launch_count() -> int:
     return int(_lib.load().pht_launch_count())

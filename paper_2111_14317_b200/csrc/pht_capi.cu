@@ -31,6 +31,7 @@ struct pht_system {
     int max_terms = 0;
     int device = 0;
     int sms = 148;
+    int dropped = 0; // terms with c = 0 removed by the packer
     double2 *d_rec = nullptr;
     int *d_off = nullptr;
     double *d_exptab = nullptr;
@@ -86,6 +87,7 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     int max_terms = 0;
     rec.reserve((size_t)M_in * RS);
     int64_t M = 0;
+    int n_dropped = 0;
     for (int k = 0; k < n; ++k) {
         std::set<std::vector<int32_t>> seen;
         int cnt = 0;
@@ -97,7 +99,7 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
             const double cr = coeffs[2 * i], ci = coeffs[2 * i + 1], w = lifting[i];
             if (!std::isfinite(cr) || !std::isfinite(ci) || !std::isfinite(w)) return PHT_EINVAL;
             if (w < 0) return PHT_ERANGE;
-            if (cr == 0.0 && ci == 0.0) continue;
+            if (cr == 0.0 && ci == 0.0) { ++n_dropped; continue; }
             for (int j = 0; j < n; ++j) rec.push_back((double)a[j]);
             rec.push_back(w);
             rec.push_back(std::log(std::hypot(cr, ci)));
@@ -128,6 +130,7 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     s->M = M;
     s->max_terms = max_terms;
     s->device = device;
+    s->dropped = n_dropped;
     cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e;
     if ((e = cudaMalloc(&s->d_rec, rec.size() * sizeof(double))) != cudaSuccess ||
@@ -310,14 +313,17 @@ extern "C" void pht_track_opts_default(pht_track_opts *o)
     o->pred_log = -1;
 }
 
-extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau, const pht_track_opts *opts,
-                         int64_t *stats, uint8_t *status, void *stream)
+static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, const double *cellw, int64_t ncells,
+                      const int32_t *path_cell, const pht_track_opts *opts, int64_t *stats, uint8_t *status,
+                      void *stream)
 {
     if (!s || p < 0 || (p > 0 && (!x || !tau || !status))) return PHT_EINVAL;
+    if (cellw && (!path_cell || ncells < 1 || ncells > INT32_MAX || s->dropped)) return PHT_EINVAL;
     if (p == 0) return PHT_OK;
     pht_track_opts o;
     if (opts) o = *opts;
     else pht_track_opts_default(&o);
+    if (cellw) o.log_state = 1; // cell coordinates w are logarithmic
     if (!(o.dtau_init > 0) || !(o.dtau_min > 0) || !(o.dtau_max > 0) || !(o.shrink > 0 && o.shrink < 1) ||
         !(o.grow >= 1) || o.newton_iters < 1 || o.grow_after < 1 || o.max_steps < 1 || o.final_iters < 0)
         return PHT_EINVAL;
@@ -336,6 +342,10 @@ extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau,
     A.status = status;
     A.stats = (long long *)stats;
     A.queue = ctr;
+    A.cellw = cellw;
+    A.path_cell = path_cell;
+    A.ncells = (int)ncells;
+    A.M = (int)s->M;
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
                          o.pred_log < 0 ? o.log_state : o.pred_log};
@@ -353,6 +363,20 @@ extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau,
     if (e2 != cudaSuccess) return cuda_fail(e2);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return PHT_OK;
+}
+
+extern "C" int pht_track(const pht_system *s, int64_t p, double *x, double *tau, const pht_track_opts *opts,
+                         int64_t *stats, uint8_t *status, void *stream)
+{
+    return track_impl(s, p, x, tau, nullptr, 0, nullptr, opts, stats, status, stream);
+}
+
+extern "C" int pht_track_cells(const pht_system *s, int64_t p, double *w, double *tau, const double *cell_lift,
+                               int64_t ncells, const int32_t *path_cell, const pht_track_opts *opts,
+                               int64_t *stats, uint8_t *status, void *stream)
+{
+    if (!cell_lift) return PHT_EINVAL;
+    return track_impl(s, p, w, tau, cell_lift, ncells, path_cell, opts, stats, status, stream);
 }
 
 extern "C" int64_t pht_launch_count(void) { return g_launches.load(); }

@@ -75,6 +75,9 @@ struct TrackArgs {
     uint8_t *status;     // [P]
     long long *stats;    // [P][4] accepted steps, rejected steps, evaluations, final iterations
     unsigned long long *queue; // path counter (zeroed by the host)
+    const double *cellw;       // optional [ncells][M] cell-shifted liftings (pht_track_cells)
+    const int *path_cell;      // [P] cell of each path
+    int ncells, M;
     TrackOpts o;
 };
 
@@ -351,9 +354,11 @@ struct RowAcc {
 
 // a2-a4 for row k of point q: row = [G_1..G_N | G_tau | h] scaled by 2^-e.
 // Terms are processed two at a time (independent dependency chains for the FP64 pipe).
+// wq (optional): per-point lifting table (cell-shifted liftings omega', pht_track_cells); the
+// term's omega is replaced by wq[i] (global term index i).
 template <int N>
 __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int k, int q,
-                                         double2 (&row)[N + 2], int &e)
+                                         double2 (&row)[N + 2], int &e, const double *wq = nullptr)
 {
     constexpr int RS = rec_stride(N);
     PointLog<N, (bool)PHT_RT_SMEM(N)> pl;
@@ -363,10 +368,12 @@ __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int
     const double2 *rec = S.rec + (size_t)i0 * (RS / 2);
     const int m = i1 - i0;
 
+    const double *wk = wq ? wq + i0 : nullptr;
     RowAcc<N> acc;
     {
         double a[RS];
         load_rec<N>(rec, a);
+        if (wk) a[N] = __ldg(wk);
         acc.init(phi_of<N>(a, pl, tau));
     }
     int i = 0;
@@ -375,6 +382,10 @@ __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int
         double a[RS], b[RS];
         load_rec<N>(rec + (size_t)i * (RS / 2), a);
         load_rec<N>(rec + (size_t)(i + 1) * (RS / 2), b);
+        if (wk) {
+            a[N] = __ldg(wk + i);
+            b[N] = __ldg(wk + i + 1);
+        }
         double pa, pb, ta, tb;
         phi_theta<N>(a, pl, tau, pa, ta);
         phi_theta<N>(b, pl, tau, pb, tb);
@@ -390,6 +401,7 @@ __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int
     for (; i < m; ++i) {
         double a[RS];
         load_rec<N>(rec + (size_t)i * (RS / 2), a);
+        if (wk) a[N] = __ldg(wk + i);
         double pa, ta;
         phi_theta<N>(a, pl, tau, pa, ta);
         const double ya = acc.reduce(pa);
@@ -715,7 +727,7 @@ struct TrackSmem {
     double nd2[N][Geo<N>::WL];   // |dx_j|^2 of this iteration
     double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL];
     long long path[Geo<N>::WL], steps[Geo<N>::WL], rej[Geo<N>::WL], evals[Geo<N>::WL], fin[Geo<N>::WL];
-    int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL];
+    int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL], cell[Geo<N>::WL];
     int acc[Geo<N>::WL];         // this iteration: 1 accept x~ -> x
     long long done_path[Geo<N>::WL]; // path finished this iteration (-1 none)
     int refill[Geo<N>::WL];      // 1: load a new path into the slot
@@ -732,8 +744,16 @@ __device__ __forceinline__ void trk_pop(TrackSmem<N> &T, const TrackArgs &A, int
             for (int u = 0; u < 4; ++u) A.stats[4 * idx + u] = 0;
         idx = atomicAdd(A.queue, 1ull);
     }
+    while ((long long)idx < A.P && A.cellw &&
+           (A.path_cell[idx] < 0 || A.path_cell[idx] >= A.ncells)) { // bad cell id: report and skip
+        A.status[idx] = (uint8_t)PT_NONFINITE;
+        if (A.stats)
+            for (int u = 0; u < 4; ++u) A.stats[4 * idx + u] = 0;
+        idx = atomicAdd(A.queue, 1ull);
+    }
     if ((long long)idx < A.P) {
         T.path[q] = (long long)idx;
+        T.cell[q] = A.cellw ? A.path_cell[idx] : 0;
         T.refill[q] = 1;
         const double t0 = A.tau[idx];
         T.tau_a[q] = t0;
@@ -809,6 +829,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
     }
     if (tid < WL) {
         T.done_path[tid] = -1;
+        T.cell[tid] = 0;
         if (tid < PTS) trk_pop<N>(T, A, tid);
         else { T.path[tid] = -1; T.refill[tid] = 0; T.phase[tid] = PH_IDLE; }
         T.acc[tid] = 0;
@@ -846,7 +867,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
         if (k < N) {
             double2 row[N + 2];
             int e;
-            eval_row<N>(S, sm, k, q, row, e);
+            const double *wq = A.cellw ? A.cellw + (size_t)T.cell[q] * A.M : nullptr;
+            eval_row<N>(S, sm, k, q, row, e, wq);
             if (q < PTS) store_row<N>(sm, k, q, row);
         }
         __syncthreads();

@@ -133,3 +133,28 @@ def test_track_log_state_noon5(P):
     rel = np.linalg.norm(xg[both] - xo[both], axis=1) / np.linalg.norm(xo[both], axis=1)
     assert rel.max() <= 1e-8, rel.max()
     assert np.sum(sg == 0) == 233
+
+
+@pytest.mark.parametrize("name", ["cyclic-5", "noon-5", "cyclic-7"])
+def test_track_cells_parity(P, name):
+    """Cell-coordinate tracking (pht_track_cells) vs the oracle's extended-range tracker with the
+    same cell-shifted liftings: identical finite counts, endpoints <= 1e-8."""
+    s = {"cyclic-5": W.cyclic(5, lift_max=100), "noon-5": W.noon(5, lift_max=1000),
+         "cyclic-7": W.cyclic(7, lift_max=10 ** 4)}[name]
+    cells = SS.mixed_cells_fast(s)
+    Wc = SS.cell_lifts(s, cells)
+    w0, tau0, cid = SS.start_points_cells(s, cells)
+    g = P.System.from_workload(s)
+    wd, td = _cuda(w0), _cuda(tau0)
+    st, stats = g.track_cells(wd, td, _cuda(Wc), _cuda(cid))
+    zg, sg = wd.cpu().numpy(), st.cpu().numpy()
+    m, e = oracle.z_to_x(w0)
+    xm, xe, to, so, sto = oracle.Oracle(s).track_x(m, e, tau0, cell_lift=Wc, path_cell=cid)
+    xo = xm * np.exp2(xe.astype(float))
+    xg = np.exp(zg)
+    assert np.sum(sg == 0) == np.sum(so == 0)
+    both = (sg == 0) & (so == 0)
+    assert both.sum() >= 0.98 * len(w0)
+    rel = np.linalg.norm(xg[both] - xo[both], axis=1) / np.linalg.norm(xo[both], axis=1)
+    assert rel.max() <= 1e-8, rel.max()
+    assert len({tuple(np.round(v, 7)) for v in xg[sg == 0]}) == np.sum(sg == 0)

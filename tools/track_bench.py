@@ -23,7 +23,13 @@ for item in which:
     sysm = CONFIGS[name](L)
     t0 = time.time()
     cells = SS.load_cells(name, L)
-    z, tau0, ids = SS.start_points_from_cells(sysm, cells)
+    CELLS = os.environ.get("TB_CELLS", "1") == "1"
+    if CELLS:
+        z, tau0, ids = SS.start_points_cells(sysm, cells)
+        wc = torch.from_numpy(SS.cell_lifts_fast(sysm, cells)).cuda()
+        cid = torch.from_numpy(ids).cuda()
+    else:
+        z, tau0, ids = SS.start_points_from_cells(sysm, cells)
     prep = time.time() - t0
     g = P.System.from_workload(sysm)
     out = {}
@@ -32,7 +38,10 @@ for item in which:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st, stats = g.track(zd, td, log_state=1, **OPTS)
+        if CELLS:
+            st, stats = g.track_cells(zd, td, wc, cid, **OPTS)
+        else:
+            st, stats = g.track(zd, td, log_state=1, **OPTS)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)

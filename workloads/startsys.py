@@ -217,7 +217,9 @@ def cell_start_points(system, cell, L: float = 37.0, tau_cap: float | None = Non
     if zmax is not None and np.max(np.abs(alpha)) > 0:
         tau0 = max(tau0, -zmax / float(np.max(np.abs(alpha))))
     Zt = Z + tau0 * alpha[None, :]
-    return np.exp(Zt), tau0, Zt
+    with np.errstate(over="ignore", under="ignore"):
+        X = np.exp(Zt)  # inf/0 where x leaves double range: use the log coordinates Zt there
+    return X, tau0, Zt
 
 
 def start_points(system, L: float = 37.0, tau_cap: float | None = None, zmax: float | None = None,
@@ -260,3 +262,68 @@ def start_points_from_cells(system, cells, L: float = 37.0):
         taus.append(np.full(len(z), t0))
         ids.append(np.full(len(z), ci))
     return np.concatenate(zs), np.concatenate(taus), np.concatenate(ids)
+
+
+def cell_lifts_fast(system, cells) -> np.ndarray:
+    """cell_lifts() with exact integer arithmetic over a common denominator per cell (numpy
+    object ints; integer liftings required)."""
+    import math
+    n, M = system.n, system.M
+    E = system.exps.astype(object)
+    w = np.array([int(v) for v in system.lifting], dtype=object)
+    eq = np.zeros(M, np.int64)
+    for k in range(n):
+        eq[system.terms_of(k)] = k
+    W = np.zeros((len(cells), M))
+    for ci, cell in enumerate(cells):
+        al = cell["alpha"]
+        D = 1
+        for a in al:
+            D = D * a.denominator // math.gcd(D, a.denominator)
+        num = np.array([int(a.numerator * (D // a.denominator)) for a in al], dtype=object)
+        val = E.dot(num) + w * D                     # (<a_i, alpha> + omega_i) * D, exact
+        beta = np.array([val[cell["pairs"][k][0]] for k in range(n)], dtype=object)
+        sh = val - beta[eq]
+        if any(v < 0 for v in sh):
+            raise RuntimeError("negative shifted lifting: not a lower cell")
+        W[ci] = [float(v) / D for v in sh]
+    return W
+
+
+def cell_lifts(system, cells) -> np.ndarray:
+    """Cell-shifted liftings omega'_i = omega_i + <a_i, alpha> - beta_k(i) of every term, per cell
+    ([ncells, M], exact rationals rounded once).  In cell coordinates x = e^{tau alpha} y the scaled
+    homotopy e^{-tau beta_k} h_k is again polyhedral with these liftings (include/pht.h
+    pht_track_cells); they are >= 0, = 0 on the cell's two terms of each equation."""
+    n = system.n
+    M = system.M
+    W = np.zeros((len(cells), M))
+    lift = [Fraction(v).limit_denominator(10**9) for v in system.lifting]
+    for ci, cell in enumerate(cells):
+        al = cell["alpha"]
+        for k in range(n):
+            p0 = cell["pairs"][k][0]
+            beta = sum(Fraction(int(system.exps[p0][j])) * al[j] for j in range(n)) + lift[p0]
+            for i in system.terms_of(k):
+                v = sum(Fraction(int(system.exps[i][j])) * al[j] for j in range(n)) + lift[i] - beta
+                if v < 0:
+                    raise RuntimeError("negative shifted lifting: not a lower cell")
+                W[ci, i] = float(v)
+    return W
+
+
+def start_points_cells(system, cells, L: float = 37.0):
+    """Start data for cell-coordinate tracking: (w0 = log y [P, n], tau0 [P], cell id [P])."""
+    n = system.n
+    ws, taus, ids = [], [], []
+    for ci, cell in enumerate(cells):
+        if cell.get("V") is None:
+            cell = dict(cell)
+            cell["V"] = [[int(system.exps[p][j]) - int(system.exps[q][j]) for j in range(n)]
+                         for (p, q) in cell["pairs"]]
+        _, t0, z = cell_start_points(system, cell, L)
+        alpha = np.array([float(a) for a in cell["alpha"]])
+        ws.append(z - t0 * alpha[None, :])
+        taus.append(np.full(len(z), t0))
+        ids.append(np.full(len(z), ci, np.int32))
+    return np.concatenate(ws), np.concatenate(taus), np.concatenate(ids)
