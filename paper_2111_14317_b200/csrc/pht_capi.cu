@@ -298,7 +298,7 @@ extern "C" void pht_track_opts_default(pht_track_opts *o)
 {
     if (!o) return;
     o->dtau_init = 0.05;
-    o->dtau_min = 1e-8;
+    o->dtau_min = 1e-12;
     o->dtau_max = 0.5;
     o->newton_tol = 1e-10;
     o->shrink = 0.5;

@@ -97,6 +97,26 @@ __device__ constexpr double INV_2PI = 0x1.45f306dc9c883p-3;
 __device__ constexpr double TWO_PI_HI = 0x1.921fb54400000p+2;
 __device__ constexpr double TWO_PI_LO = 0x1.0b4611a626331p-32;
 
+// Polynomial / reduction constants as a __constant__ table: the compiler then feeds them to DFMA
+// as constant-bank operands instead of materialising each 64-bit immediate with two UMOVs.
+__constant__ double KC[16] = {
+    0x1.71547652b82fep+8,  // 0 256/ln2
+    0x1.62e42fee00000p-9,  // 1 ln2/256 hi
+    0x1.a39ef35793c76p-41, // 2 ln2/256 lo
+    1.0 / 24.0,            // 3
+    1.0 / 6.0,             // 4
+    0x1.45f306dc9c883p+5,  // 5 256/(2pi)
+    0x1.921fb54400000p-6,  // 6 C1
+    0x1.0b4611a600000p-40, // 7 C2
+    0x1.3198a2e037073p-75, // 8 C3
+    1.0 / 120.0,           // 9
+    -1.0 / 6.0,            // 10
+    -1.0 / 720.0,          // 11
+    0x1.62e42fee00000p-1,  // 12 ln2 hi
+    0x1.a39ef35793c76p-33, // 13 ln2 lo
+    0x1.71547652b82fep+0,  // 14 1/ln2
+    0.0};
+
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
@@ -152,26 +172,26 @@ __device__ __forceinline__ void log_split(double2 x, double &rho, double &th, do
 // the reduced arguments (|r| <= ln2/512, |s| <= pi/256); error <= ~4 ulp.
 __device__ __forceinline__ double2 expcis(double y, double th, const double *etab, const double2 *ctab)
 {
-    const double kf = fma(y, K256_LN2, SHIFT);
+    const double kf = fma(y, KC[0], SHIFT);
     const int ki = __double2loint(kf);
     const double kd = kf - SHIFT;
-    double r = fma(kd, -LN2_256_HI, y);
-    r = fma(kd, -LN2_256_LO, r);
-    const double p = fma(fma(fma(fma(r, 1.0 / 24.0, 1.0 / 6.0), r, 0.5), r, 1.0), r, 1.0);
+    double r = fma(kd, -KC[1], y);
+    r = fma(kd, -KC[2], r);
+    const double p = fma(fma(fma(fma(r, KC[3], KC[4]), r, 0.5), r, 1.0), r, 1.0);
     double mag = etab[ki & 255] * p;
     const int m = ki >> 8;
     const unsigned hi = (unsigned)__double2hiint(mag) + ((unsigned)m << 20);
     mag = (m < -1000) ? 0.0 : __hiloint2double((int)hi, __double2loint(mag));
 
-    const double qf = fma(th, K256_2PI, SHIFT);
+    const double qf = fma(th, KC[5], SHIFT);
     const int qi = __double2loint(qf);
     const double qd = qf - SHIFT;
-    double s = fma(qd, -C1, th);
-    s = fma(qd, -C2, s);
-    s = fma(qd, -C3, s);
+    double s = fma(qd, -KC[6], th);
+    s = fma(qd, -KC[7], s);
+    s = fma(qd, -KC[8], s);
     const double s2 = s * s;
-    const double sn = fma(s * s2, fma(s2, 1.0 / 120.0, -1.0 / 6.0), s);
-    const double cs = fma(s2, fma(s2, fma(s2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+    const double sn = fma(s * s2, fma(s2, KC[9], KC[10]), s);
+    const double cs = fma(s2, fma(s2, fma(s2, KC[11], KC[3]), -0.5), 1.0);
     const double2 T = ctab[qi & 255];
     const double cr = fma(T.x, cs, -T.y * sn);
     const double ci = fma(T.y, cs, T.x * sn);
@@ -209,7 +229,9 @@ struct Geo {
 
 template <int N>
 struct Smem {
-    static constexpr int WL = Geo<N>::WL;
+    // [variable][point] tiles use a row stride of WL + 1 (odd in 16-byte units): accesses with
+    // consecutive threads on consecutive variables of a point are then bank-conflict free.
+    static constexpr int WL = Geo<N>::WL + 1;
     double exptab[256];
     double2 cistab[256];
     double2 rt[N][WL];    // (rho, vartheta) per variable
@@ -217,11 +239,11 @@ struct Smem {
     double2 inv[N][WL];   // 1/x (EVAL_X); staging of dE (DIRS)
     double2 out2[N][WL];  // staging of dN (DIRS)
     double dn2[N][WL];
-    double tau[WL];
-    double tinv[WL];
-    int st[WL];
-    unsigned keys[Geo<N>::NWARP][Geo<N>::PPW * Geo<N>::KS]; // pivot keys (L layout)
-    double2 mat[Geo<N>::PTS * Geo<N>::MS]; // [q][row][col]: solve tile / staged evaluate output
+    double tau[Geo<N>::WL];
+    double tinv[Geo<N>::WL];
+    int st[Geo<N>::WL];
+    alignas(16) unsigned keys[Geo<N>::NWARP][Geo<N>::PPW * Geo<N>::KS]; // pivot keys (L layout)
+    alignas(16) double2 mat[Geo<N>::PTS * Geo<N>::MS]; // [q][row][col]: solve tile / staged output
 };
 
 // Term record -> registers: a_0..a_{N-1}, omega, log|c|, arg c (pht_capi.cu packer).
@@ -314,20 +336,20 @@ struct RowAcc {
 #pragma unroll
         for (int j = 0; j < N; ++j) g[j] = make_double2(0.0, 0.0);
         gt = h = make_double2(0.0, 0.0);
-        set_exp(rint(phi0 * INV_LN2));
+        set_exp(rint(phi0 * KC[14]));
     }
     __device__ __forceinline__ void set_exp(double e)
     {
         ed = e;
-        eh = e * LN2_HI;
-        el = e * LN2_LO;
+        eh = e * KC[12];
+        el = e * KC[13];
     }
     __device__ __forceinline__ double reduced(double phi) const { return (phi - eh) - el; }
     __device__ __forceinline__ double reduce(double phi)
     {
         double y = (phi - eh) - el;
         if (y > 512.0) { // rare: rescale everything to the new leading term (exact power of two)
-            const double e2 = rint(phi * INV_LN2);
+            const double e2 = rint(phi * KC[14]);
             const double f = scalbn(1.0, (int)fmax(ed - e2, -2000.0));
 #pragma unroll
             for (int j = 0; j < N; ++j) g[j] = make_double2(g[j].x * f, g[j].y * f);
@@ -362,7 +384,7 @@ __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int
 {
     constexpr int RS = rec_stride(N);
     PointLog<N, (bool)PHT_RT_SMEM(N)> pl;
-    pl.template load<Geo<N>::WL>(sm.rt, q);
+    pl.template load<Smem<N>::WL>(sm.rt, q);
     const double tau = sm.tau[q];
     const int i0 = __ldg(S.off + k), i1 = __ldg(S.off + k + 1);
     const double2 *rec = S.rec + (size_t)i0 * (RS / 2);
@@ -492,16 +514,25 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
     for (int j = 0; j < N; ++j) {
         unsigned key = 0u;
         if (!used) key = ((unsigned)__double2hiint(cabs1(a[j])) & ~63u) | (unsigned)(32 - i);
-        if (act) kseg[i] = key;
-        __syncwarp();
         unsigned kmax = 0u;
+        if (PPW <= 4) {
+            // one full-warp redux per point segment (uniform datapath, no divergence)
 #pragma unroll
-        for (int u = 0; u < KS; u += 4) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(kseg + u);
-            kmax = max(kmax, (u + 0 < N) ? v.x : 0u);
-            kmax = max(kmax, (u + 1 < N) ? v.y : 0u);
-            kmax = max(kmax, (u + 2 < N) ? v.z : 0u);
-            kmax = max(kmax, (u + 3 < N) ? v.w : 0u);
+            for (int sg = 0; sg < PPW; ++sg) {
+                const unsigned m = __reduce_max_sync(0xffffffffu, (seg0 == sg) ? key : 0u);
+                kmax = (seg == sg) ? m : kmax;
+            }
+        } else {
+            if (act) kseg[i] = key;
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < KS; u += 4) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(kseg + u);
+                kmax = max(kmax, (u + 0 < N) ? v.x : 0u);
+                kmax = max(kmax, (u + 1 < N) ? v.y : 0u);
+                kmax = max(kmax, (u + 2 < N) ? v.z : 0u);
+                kmax = max(kmax, (u + 3 < N) ? v.w : 0u);
+            }
         }
         const int r = 32 - (int)(kmax & 63u);
         const bool me = (i == r);
@@ -721,10 +752,10 @@ enum : int { PH_IDLE = 0, PH_PREDICT = 1, PH_CORRECT = 2, PH_FINAL = 3 };
 template <int N>
 struct TrackSmem {
     Smem<N> s;
-    double2 xa[N][Geo<N>::WL];   // accepted point
-    double2 xt[N][Geo<N>::WL];   // trial point
-    double2 dd[N][Geo<N>::WL];   // direction of this iteration (delta_E or delta_N, log coords)
-    double nd2[N][Geo<N>::WL];   // |dx_j|^2 of this iteration
+    double2 xa[N][Geo<N>::WL + 1];   // accepted point (padded rows: see Smem)
+    double2 xt[N][Geo<N>::WL + 1];   // trial point
+    double2 dd[N][Geo<N>::WL + 1];   // direction of this iteration (delta_E or delta_N, log coords)
+    double nd2[N][Geo<N>::WL + 1];   // |dx_j / x_j|^2 of this iteration
     double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL];
     long long path[Geo<N>::WL], steps[Geo<N>::WL], rej[Geo<N>::WL], evals[Geo<N>::WL], fin[Geo<N>::WL];
     int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL], cell[Geo<N>::WL];
