@@ -165,7 +165,7 @@ int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
  */
 typedef struct {
     double dtau_init;   /* 0.05   initial step in tau                                   */
-    double dtau_min;    /* 1e-8   step underflow threshold                              */
+    double dtau_min;    /* 1e-12  step underflow threshold (events sit at |tau| ~ 1/omega)  */
     double dtau_max;    /* 0.5                                                           */
     double newton_tol;  /* 1e-10  corrector: max_j |dN_j|/|x_j| <= newton_tol             */
     double shrink;      /* 0.5                                                           */

@@ -134,7 +134,7 @@ class Oracle:
         assert rc == 0
         return x, tau, st, dn
 
-    def track(self, x, tau, *, dtau_init=0.05, dtau_min=1e-8, dtau_max=0.5, newton_tol=1e-10,
+    def track(self, x, tau, *, dtau_init=0.05, dtau_min=1e-12, dtau_max=0.5, newton_tol=1e-10,
               shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
               max_steps=10000, final_iters=5, pred_log=0):
         x = _c2(x).copy()
@@ -150,7 +150,7 @@ class Oracle:
         return x, tau, st, stats
 
 
-    def track_x(self, xm, xe, tau, *, dtau_init=0.05, dtau_min=1e-8, dtau_max=0.5, newton_tol=1e-10,
+    def track_x(self, xm, xe, tau, *, dtau_init=0.05, dtau_min=1e-12, dtau_max=0.5, newton_tol=1e-10,
                 shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
                 max_steps=10000, final_iters=5, pred_log=1, cell_lift=None, path_cell=None):
         """orc_track_x: the tracker with extended-range state x = xm * 2**xe; with cell_lift
