@@ -172,6 +172,10 @@ __device__ __forceinline__ void log_split(double2 x, double &rho, double &th, do
 // the reduced arguments (|r| <= ln2/512, |s| <= pi/256); error <= ~4 ulp.
 __device__ __forceinline__ double2 expcis(double y, double th, const double *etab, const double2 *ctab)
 {
+    // terms more than e^-2000 below the row scale flush to 0; clamping first keeps y*256/ln2
+    // inside the 32-bit integer extracted from the shifter (|y| up to ~10^8 occurs for large
+    // cell-shifted liftings)
+    y = fmax(y, -2000.0);
     const double kf = fma(y, KC[0], SHIFT);
     const int ki = __double2loint(kf);
     const double kd = kf - SHIFT;

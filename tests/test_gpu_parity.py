@@ -254,3 +254,18 @@ def test_evaluate_log_extreme_rows(P, name, n):
             worst = max(worst, abs(got - ref))
     # a-priori bound (reading R9/A27): ~2.7 u * max|phi| ~ 1e-12 here
     assert worst <= 1e-10, worst
+
+
+def test_evaluate_vanishing_terms_huge_lifting(P):
+    """A term with tau*omega ~ -1e7 (far below the row) must vanish, not wrap the exponent:
+    h = x1 - t^(10^7) x2 at tau = -1 equals x1 (regression: 32-bit overflow in the exp reduction)."""
+    sysm = W.from_terms("huge", 2, [[((1, 0), 1.0, 0), ((0, 1), -1.0, 10**7)], [((0, 1), 1.0, 0), ((0, 0), -2.0, 0)]],
+                        coeffs="native")
+    g = P.System.from_workload(sysm)
+    z = np.array([[0.3 + 0.2j, 0.1 - 0.4j]] * 4)
+    tau = np.array([-1.0, -3.0, -0.5, -2.0])
+    H, Jz, Jtau, e2, st = g.evaluate_log(_cuda(z), _cuda(tau))
+    H = H.cpu().numpy() * np.exp2(e2.cpu().numpy().astype(float))
+    assert np.allclose(H[:, 0], np.exp(z[:, 0]), rtol=1e-14, atol=0)
+    o = oracle.Oracle(sysm).evaluate(np.exp(z), np.exp(tau))
+    assert np.allclose(H, o["H"], rtol=1e-14, atol=1e-300)

@@ -158,3 +158,43 @@ def test_track_cells_parity(P, name):
     rel = np.linalg.norm(xg[both] - xo[both], axis=1) / np.linalg.norm(xo[both], axis=1)
     assert rel.max() <= 1e-8, rel.max()
     assert len({tuple(np.round(v, 7)) for v in xg[sg == 0]}) == np.sum(sg == 0)
+
+
+def _cells_parity_on(P, name, L, sample=None, seed=0):
+    from workloads.make_starts import CONFIGS
+    s = CONFIGS[name](L)
+    cells = SS.load_cells(name, L)
+    Wc = SS.cell_lifts_fast(s, cells)
+    w0, tau0, cid = SS.start_points_cells(s, cells)
+    if sample is not None:
+        pick = np.sort(np.random.default_rng(seed).choice(len(w0), sample, replace=False))
+        w0, tau0, cid = w0[pick], tau0[pick], cid[pick]
+    g = P.System.from_workload(s)
+    wd, td = _cuda(w0), _cuda(tau0)
+    st, _ = g.track_cells(wd, td, _cuda(Wc), _cuda(cid))
+    zg, sg = wd.cpu().numpy(), st.cpu().numpy()
+    m, e = oracle.z_to_x(w0)
+    xm, xe, _, so, _ = oracle.Oracle(s).track_x(m, e, tau0, cell_lift=Wc, path_cell=cid)
+    return np.exp(zg), sg, xm * np.exp2(xe.astype(float)), so
+
+
+def test_track_cells_katsura10_all_paths(P):
+    """BASELINE.json configs[1]: every katsura-10 start path (990 = torus mixed volume) on the GPU
+    vs the extended-range oracle tracker: identical finite counts, endpoints <= 1e-8."""
+    xg, sg, xo, so = _cells_parity_on(P, "katsura-10", 10_000)
+    assert len(xg) == 990
+    assert np.sum(sg == 0) == np.sum(so == 0) == 990
+    rel = np.linalg.norm(xg - xo, axis=1) / np.linalg.norm(xo, axis=1)
+    assert rel.max() <= 1e-8, rel.max()
+
+
+@pytest.mark.parametrize("name,L", [("noon-10", 10_000), ("cyclic-10", 1_000_000)])
+def test_track_cells_sampled_paths(P, name, L):
+    """Seeded 256-path samples of the noon-10 / cyclic-10 start systems: same statuses and
+    endpoints <= 1e-8 on paths both trackers finish."""
+    xg, sg, xo, so = _cells_parity_on(P, name, L, sample=256, seed=3)
+    assert np.sum(sg == 0) == np.sum(so == 0)
+    both = (sg == 0) & (so == 0)
+    assert both.sum() >= 250
+    rel = np.linalg.norm(xg[both] - xo[both], axis=1) / np.linalg.norm(xo[both], axis=1)
+    assert rel.max() <= 1e-8, rel.max()
