@@ -26,6 +26,7 @@ SIGNATURES = {
     "pht_system_create": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(_vp)]),
     "pht_system_destroy": (None, [_vp]),
     "pht_system_info": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pht_system_flags": (ctypes.c_int, [_vp]),
     "pht_evaluate": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_evaluate_log": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_euler_newton": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -45,6 +45,7 @@ class System:
         check(lib.pht_system_info(h, ctypes.byref(nn), ctypes.byref(M), ctypes.byref(mt), ctypes.byref(dev)),
               "pht_system_info")
         self.n, self.M, self.max_terms = nn.value, M.value, mt.value
+        self.dense = bool(lib.pht_system_flags(h) & 1)  # FP64 tensor-core evaluation path
 
     @classmethod
     def from_workload(cls, system, device: int = 0):

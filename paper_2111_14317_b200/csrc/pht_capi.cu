@@ -1,10 +1,12 @@
 // pht_capi.cu — C ABI (include/pht.h): system loader / packer (the
 // paper's Alg. 1 "Initialize") and the entry points that enqueue k_pht.
 #include "../../include/pht.h"
+#include "pht_dense.cuh"
 #include "pht_kernels.cuh"
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -15,7 +17,8 @@
 namespace pht {
 #define PHT_DECL(N)                                                                             \
     extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t);     \
-    extern template cudaError_t launch_track<N>(const DevSys &, const TrackArgs &, cudaStream_t, int);
+    extern template cudaError_t launch_track<N>(const DevSys &, const TrackArgs &, cudaStream_t, int); \
+    extern template cudaError_t launch_dense<N>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t);
 PHT_DECL(1) PHT_DECL(2) PHT_DECL(3) PHT_DECL(4) PHT_DECL(5) PHT_DECL(6) PHT_DECL(7) PHT_DECL(8)
 PHT_DECL(9) PHT_DECL(10) PHT_DECL(11) PHT_DECL(12) PHT_DECL(13) PHT_DECL(14) PHT_DECL(15)
 PHT_DECL(16) PHT_DECL(17) PHT_DECL(18) PHT_DECL(19) PHT_DECL(20) PHT_DECL(21) PHT_DECL(22)
@@ -36,6 +39,10 @@ struct pht_system {
     int *d_off = nullptr;
     double *d_exptab = nullptr;
     double2 *d_cistab = nullptr;
+    // dense FP64 tensor-core path (pht_dense.cuh), built when the system is genuinely dense
+    int dense = 0;
+    double *d_b2phi = nullptr, *d_b2th = nullptr, *d_b4 = nullptr;
+    int *d_ntoff = nullptr;
     // workspace for the *_host entry points
     std::mutex ws_mu;
     int64_t ws_cap = 0;
@@ -144,6 +151,71 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
         pht_system_destroy(s);
         return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
     }
+    // dense policy: n >= 12 and at least half of the exponent entries nonzero (config C4),
+    // overridable with PHT_DENSE=0/1 (experiments)
+    {
+        int64_t nnz = 0;
+        for (int64_t i = 0; i < M_in; ++i)
+            for (int j = 0; j < n; ++j) nnz += exps[i * n + j] != 0;
+        int want = (n >= 12 && n_dropped == 0 && 2 * nnz >= M_in * n) ? 1 : 0;
+        if (const char *ev = getenv("PHT_DENSE")) want = (ev[0] == '1') && n_dropped == 0;
+        if (want) {
+            const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;
+            std::vector<int> ntoff(n + 1, 0);
+            for (int k = 0; k < n; ++k) ntoff[k + 1] = ntoff[k] + (int)((off[k + 1] - off[k] + 7) / 8);
+            const int NT = ntoff[n];
+            std::vector<double> b2p((size_t)NT * KS * 32), b2t((size_t)NT * KS * 32), b4((size_t)2 * NT * CT * 32);
+            for (int k = 0; k < n; ++k) {
+                for (int t = 0; t < ntoff[k + 1] - ntoff[k]; ++t) {
+                    const int ntg = ntoff[k] + t;
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int g = lane >> 2, r = lane & 3;
+                        const int64_t i = off[k] + 8 * t + g; // stage 2: B[r][g] = term 8t+g
+                        const bool real = i < off[k + 1];
+                        for (int kk = 0; kk < KS; ++kk) {
+                            const int kr = 4 * kk + r;
+                            double vp = 0.0, vt = 0.0;
+                            if (real) {
+                                const double cr = coeffs[2 * i], ci = coeffs[2 * i + 1];
+                                if (kr < n) vp = vt = exps[i * n + kr];
+                                else if (kr == n) vp = lifting[i];
+                                else if (kr == n + 1) { vp = std::log(std::hypot(cr, ci)); vt = std::atan2(ci, cr); }
+                            } else if (kr == n + 1) {
+                                vp = -1e300; // padding term: exp -> 0
+                            }
+                            b2p[((size_t)ntg * KS + kk) * 32 + lane] = vp;
+                            b2t[((size_t)ntg * KS + kk) * 32 + lane] = vt;
+                        }
+                        for (int h = 0; h < 2; ++h) { // stage 4: B[r][g] = term 8t+4h+r, column 8ct+g
+                            const int64_t i4 = off[k] + 8 * t + 4 * h + r;
+                            for (int ct = 0; ct < CT; ++ct) {
+                                const int c = 8 * ct + g;
+                                double v = 0.0;
+                                if (i4 < off[k + 1]) {
+                                    if (c < n) v = exps[i4 * n + c];
+                                    else if (c == n) v = lifting[i4];
+                                    else if (c == n + 1) v = 1.0;
+                                }
+                                b4[((size_t)(2 * ntg + h) * CT + ct) * 32 + lane] = v;
+                            }
+                        }
+                    }
+                }
+            }
+            if ((e = cudaMalloc(&s->d_b2phi, b2p.size() * 8)) != cudaSuccess ||
+                (e = cudaMalloc(&s->d_b2th, b2t.size() * 8)) != cudaSuccess ||
+                (e = cudaMalloc(&s->d_b4, b4.size() * 8)) != cudaSuccess ||
+                (e = cudaMalloc(&s->d_ntoff, ntoff.size() * sizeof(int))) != cudaSuccess ||
+                (e = cudaMemcpy(s->d_b2phi, b2p.data(), b2p.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(s->d_b2th, b2t.data(), b2t.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(s->d_b4, b4.data(), b4.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(s->d_ntoff, ntoff.data(), ntoff.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess) {
+                pht_system_destroy(s);
+                return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
+            }
+            s->dense = 1;
+        }
+    }
     *out = s;
     return PHT_OK;
 }
@@ -156,6 +228,10 @@ extern "C" void pht_system_destroy(pht_system *s)
     cudaFree(s->d_off);
     cudaFree(s->d_exptab);
     cudaFree(s->d_cistab);
+    cudaFree(s->d_b2phi);
+    cudaFree(s->d_b2th);
+    cudaFree(s->d_b4);
+    cudaFree(s->d_ntoff);
     cudaFree(s->ws);
     delete s;
 }
@@ -171,6 +247,12 @@ extern "C" int pht_system_info(const pht_system *s, int32_t *n, int64_t *M, int3
     return PHT_OK;
 }
 
+extern "C" int pht_system_flags(const pht_system *s)
+{
+    if (!s) return PHT_EINVAL;
+    return s->dense ? PHT_SYS_DENSE : 0;
+}
+
 static int dispatch(const pht_system *s, int mode, const pht::Args &A, void *stream)
 {
     if (A.P == 0) return PHT_OK;
@@ -179,8 +261,10 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A, void *str
     pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
+    const bool dense = s->dense && (mode == pht::MODE_EVAL_X || mode == pht::MODE_EVAL_Z);
+    const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff};
     switch (s->n) {
-#define PHT_CASE(N) case N: e = pht::launch<N>(mode, S, A, st); break;
+#define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
         PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12) PHT_CASE(13) PHT_CASE(14)
         PHT_CASE(15) PHT_CASE(16) PHT_CASE(17) PHT_CASE(18) PHT_CASE(19) PHT_CASE(20) PHT_CASE(21)

@@ -1,0 +1,285 @@
+// pht_dense.cuh — FP64 tensor-core (DMMA) evaluation for genuinely dense systems.
+//
+// BASELINE.json north_star: stage 2 "forms the monomial exponents as dense products of the
+// stacked integer exponent/lifting matrix [A; omega] against the log-point matrix ... FP64
+// tensor-core DMMA tiles only where the contraction is genuinely dense" (config C4: random dense
+// Laurent n=20, 50 terms per equation).  sm_100a has no f64 tcgen05 kind; FP64 tensor work is
+// mma.sync.m8n8k4.f64 (SASS DMMA), measured at 37.1 TFLOP/s on B200 (profiles/r01_microbench).
+//
+// Per warp: NMT M-tiles of 8 points.  Per equation k, its terms are streamed in n-tiles of 8:
+//   stage 2  Phi(8 pts x 8 terms)   = [rho | tau | 1 | 0]   (8 x KP) . B_phi(KP x 8)   (DMMA)
+//            Theta(8 pts x 8 terms) = [theta | 0 | 1 | 0] (8 x KP) . B_th (KP x 8)    (DMMA)
+//            with B_phi rows = (a_i, omega_i, log|c_i|), B_th rows = (a_i, 0, arg c_i)
+//   stage 3  w = exp(phi - e ln2) cis(theta) on the accumulator fragments; e = per-point online
+//            row exponent (quad shuffles; exact power-of-two rescale of the accumulators, R7)
+//   stage 4  [G_1..G_N | G_tau | h](8 x CT*8) += W(8 x 4) . B4(4 x 8) per 4-term k-step, real
+//            and imaginary parts of W as separate A operands; B4 rows = (a_i, omega_i, 1)
+//            ("e^{z A} B_k^T").  W moves from accumulator to operand layout with
+//            quad shuffles.
+// B operands are pre-swizzled on the host into fragment order: one coalesced 256-byte load per
+// (tile, k-step) per warp, reused for all NMT M-tiles.
+// Fragment layouts of mma.m8n8k4 f64 (lane = 4*g + r): A(8x4): A[g][r]; B(4x8): B[r][g];
+// C(8x8): C[g][2r], C[g][2r+1].
+#pragma once
+
+#include "pht_kernels.cuh"
+
+namespace pht {
+
+struct DenseSys {
+    const double *b2phi;   // [sum_k ntk][KS][32]
+    const double *b2th;    // [sum_k ntk][KS][32]
+    const double *b4;      // [sum_k 2*ntk][CT][32]
+    const int *ntile_off;  // [n+1] prefix sums of ntk (n-tiles of 8 terms per equation)
+};
+
+template <int N>
+struct DGeo {
+    static constexpr int KP = (N + 2 + 3) & ~3; // stage-2 K (vars + tau/const) padded to 4
+    static constexpr int KS = KP / 4;          // stage-2 k-steps
+    static constexpr int CT = (N + 2 + 7) / 8; // stage-4 column tiles of 8
+    static constexpr int NMT = 2;              // M-tiles (8 points) per warp
+    static constexpr int WARPS = 4;
+    static constexpr int PTS = WARPS * NMT * 8; // points per CTA
+};
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int N>
+struct DenseSmem {
+    double exptab[256];
+    double2 cistab[256];
+    double ap[DGeo<N>::PTS][DGeo<N>::KP + 1]; // A operand rows for phi: rho_j, tau, 1
+    double at[DGeo<N>::PTS][DGeo<N>::KP + 1]; // A operand rows for theta: theta_j, 0, 1
+    double2 inv[DGeo<N>::PTS][N + 1];         // 1/x (EVAL_X)
+    double tinv[DGeo<N>::PTS];
+    int st[DGeo<N>::PTS];
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 2) k_dense(const DevSys S, const DenseSys D, const Args A)
+{
+    using G = DGeo<N>;
+    constexpr int KP = G::KP, KS = G::KS, CT = G::CT, NMT = G::NMT, PTS = G::PTS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DenseSmem<N> &sm = *reinterpret_cast<DenseSmem<N> *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, r = lane & 3; // fragment coordinates
+    for (int i = tid; i < 256; i += G::WARPS * 32) {
+        sm.exptab[i] = __ldg(S.exptab + i);
+        sm.cistab[i] = __ldg(S.cistab + i);
+    }
+    const int64_t base = (int64_t)blockIdx.x * PTS;
+    for (int q = tid; q < PTS; q += G::WARPS * 32) sm.st[q] = 0;
+    __syncthreads();
+    // stage 1: log split of every (point, variable) of the tile, plus tau
+    for (int e = tid; e < PTS * N; e += G::WARPS * 32) {
+        const int q = e / N, j = e - q * N;
+        double rho = 0.0, th = 0.0;
+        int st = 0;
+        if (base + q < A.P) {
+            const double2 v = A.xin[(base + q) * N + j];
+            if (MODE == MODE_EVAL_Z) {
+                if (!(isfinite(v.x) && isfinite(v.y))) st |= PT_NONFINITE;
+                else {
+                    rho = v.x;
+                    const double kq = rint(v.y * INV_2PI);
+                    th = fma(-kq, TWO_PI_LO, fma(-kq, TWO_PI_HI, v.y));
+                }
+            } else {
+                double2 inv;
+                log_split(v, rho, th, inv, st);
+                sm.inv[q][j] = inv;
+            }
+        }
+        sm.ap[q][j] = rho;
+        sm.at[q][j] = th;
+        if (st) atomicOr(&sm.st[q], st);
+    }
+    for (int q = tid; q < PTS; q += G::WARPS * 32) {
+        double tau = 0.0;
+        int st = 0;
+        sm.tinv[q] = 1.0;
+        if (base + q < A.P) {
+            const double tv = A.tin[base + q];
+            if (MODE == MODE_EVAL_Z) {
+                tau = tv;
+                if (!isfinite(tv)) { st |= PT_NONFINITE; tau = 0.0; }
+            } else {
+                if (!(tv > 0.0) || !isfinite(tv)) st |= PT_NONFINITE;
+                else { tau = log(tv); sm.tinv[q] = 1.0 / tv; }
+            }
+        }
+        for (int c = N; c < KP; ++c) {
+            sm.ap[q][c] = (c == N) ? tau : (c == N + 1 ? 1.0 : 0.0);
+            sm.at[q][c] = (c == N + 1) ? 1.0 : 0.0;
+        }
+        if (st) atomicOr(&sm.st[q], st);
+    }
+    __syncthreads();
+    // A fragments (constant over equations): thread holds A[point 8m+g][col 4kk+r]
+    double aP[NMT][KS], aT[NMT][KS];
+#pragma unroll
+    for (int m = 0; m < NMT; ++m) {
+        const int q = (warp * NMT + m) * 8 + g;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            aP[m][kk] = sm.ap[q][4 * kk + r];
+            aT[m][kk] = sm.at[q][4 * kk + r];
+        }
+    }
+    const bool scaled = A.rexp != nullptr;
+
+    for (int k = 0; k < N; ++k) {
+        const int nt0 = __ldg(D.ntile_off + k), nt1 = __ldg(D.ntile_off + k + 1);
+        // stage-4 accumulators [m][ct][re/im][2]
+        double acc[NMT][CT][2][2];
+        double ed[NMT], eh[NMT], el[NMT]; // per-point row exponent (this thread's row g)
+#pragma unroll
+        for (int m = 0; m < NMT; ++m) {
+            ed[m] = -1e300;
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct)
+                acc[m][ct][0][0] = acc[m][ct][0][1] = acc[m][ct][1][0] = acc[m][ct][1][1] = 0.0;
+        }
+        for (int nt = nt0; nt < nt1; ++nt) {
+            // stage 2: phi and theta tiles for the 8 terms of this n-tile
+            double ph[NMT][2], th[NMT][2];
+#pragma unroll
+            for (int m = 0; m < NMT; ++m) ph[m][0] = ph[m][1] = th[m][0] = th[m][1] = 0.0;
+            const double *bp = D.b2phi + ((size_t)nt * KS) * 32 + lane;
+            const double *bt = D.b2th + ((size_t)nt * KS) * 32 + lane;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+                const double vp = __ldg(bp + kk * 32), vt = __ldg(bt + kk * 32);
+#pragma unroll
+                for (int m = 0; m < NMT; ++m) {
+                    dmma(ph[m][0], ph[m][1], aP[m][kk], vp);
+                    dmma(th[m][0], th[m][1], aT[m][kk], vt);
+                }
+            }
+            // stage 3: online row exponent per point (row g is shared by the quad) and exp*cis
+            double wr[NMT][2], wi[NMT][2];
+#pragma unroll
+            for (int m = 0; m < NMT; ++m) {
+                double mx = fmax(ph[m][0], ph[m][1]);
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                if (ed[m] == -1e300) { // first n-tile: set the exponent from the leading term
+                    ed[m] = isfinite(mx) ? rint(mx * KC[14]) : 0.0;
+                    eh[m] = ed[m] * KC[12];
+                    el[m] = ed[m] * KC[13];
+                } else if ((mx - eh[m]) - el[m] > 512.0) { // exact power-of-two rescale
+                    const double e2 = rint(mx * KC[14]);
+                    const double f = scalbn(1.0, (int)fmax(ed[m] - e2, -2000.0));
+#pragma unroll
+                    for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            acc[m][ct][u][0] *= f;
+                            acc[m][ct][u][1] *= f;
+                        }
+                    ed[m] = e2;
+                    eh[m] = e2 * KC[12];
+                    el[m] = e2 * KC[13];
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const double2 w = expcis((ph[m][u] - eh[m]) - el[m], th[m][u], sm.exptab, sm.cistab);
+                    wr[m][u] = w.x;
+                    wi[m][u] = w.y;
+                }
+            }
+            // stage 4: two k-steps of 4 terms; A operand W[row g][term 4h + r] from the quad
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int jt = 4 * h + r;              // term of this lane's A element
+                const int src = (lane & ~3) | (jt >> 1); // quad lane holding it
+                const double *b4 = D.b4 + ((size_t)(2 * nt + h) * CT) * 32 + lane;
+                double bv[CT];
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct) bv[ct] = __ldg(b4 + ct * 32);
+#pragma unroll
+                for (int m = 0; m < NMT; ++m) {
+                    const double r0 = __shfl_sync(0xffffffffu, wr[m][0], src);
+                    const double r1 = __shfl_sync(0xffffffffu, wr[m][1], src);
+                    const double i0 = __shfl_sync(0xffffffffu, wi[m][0], src);
+                    const double i1 = __shfl_sync(0xffffffffu, wi[m][1], src);
+                    const double ar = (jt & 1) ? r1 : r0, ai = (jt & 1) ? i1 : i0;
+#pragma unroll
+                    for (int ct = 0; ct < CT; ++ct) {
+                        dmma(acc[m][ct][0][0], acc[m][ct][0][1], ar, bv[ct]);
+                        dmma(acc[m][ct][1][0], acc[m][ct][1][1], ai, bv[ct]);
+                    }
+                }
+            }
+        }
+        // epilogue for equation k: this thread holds columns 8ct + 2r + {0,1} of point row g
+#pragma unroll
+        for (int m = 0; m < NMT; ++m) {
+            const int q = (warp * NMT + m) * 8 + g;
+            const int64_t gq = base + q;
+            const int e = (int)ed[m];
+            bool fin = true;
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int c = 8 * ct + 2 * r + u;
+                    if (c >= N + 2) continue;
+                    double2 v = make_double2(acc[m][ct][0][u], acc[m][ct][1][u]);
+                    if (MODE == MODE_EVAL_X) {
+                        if (c < N) v = cmul(v, sm.inv[q][c]);
+                        else if (c == N) v = make_double2(v.x * sm.tinv[q], v.y * sm.tinv[q]);
+                    }
+                    if (!scaled && e != 0) v = make_double2(scalbn(v.x, e), scalbn(v.y, e));
+                    fin = fin && isfinite(v.x) && isfinite(v.y);
+                    if (gq < A.P) {
+                        if (c < N) { if (A.J) A.J[(gq * N + k) * N + c] = v; }
+                        else if (c == N) { if (A.Jt) A.Jt[gq * N + k] = v; }
+                        else if (A.H) A.H[gq * N + k] = v;
+                    }
+                }
+            if (!fin) atomicOr(&sm.st[q], PT_NONFINITE);
+            if (scaled && r == 0 && gq < A.P) A.rexp[gq * N + k] = e;
+        }
+    }
+    __syncthreads();
+    for (int q = tid; q < PTS; q += G::WARPS * 32)
+        if (base + q < A.P && A.status) A.status[base + q] = (uint8_t)sm.st[q];
+}
+
+template <int N, int MODE>
+cudaError_t launch_dense_mode(const DevSys &S, const DenseSys &D, const Args &A, cudaStream_t stream)
+{
+    constexpr int PTS = DGeo<N>::PTS;
+    const int64_t tiles = (A.P + PTS - 1) / PTS;
+    if (tiles == 0) return cudaSuccess;
+    const size_t sb = sizeof(DenseSmem<N>);
+    static std::atomic<unsigned long long> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(k_dense<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        if (e != cudaSuccess) return e;
+        configured.fetch_or(bit);
+    }
+    k_dense<N, MODE><<<dim3((unsigned)tiles), dim3(DGeo<N>::WARPS * 32), sb, stream>>>(S, D, A);
+    return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_dense(int mode, const DevSys &S, const DenseSys &D, const Args &A, cudaStream_t stream)
+{
+    if (mode == MODE_EVAL_X) return launch_dense_mode<N, MODE_EVAL_X>(S, D, A, stream);
+    if (mode == MODE_EVAL_Z) return launch_dense_mode<N, MODE_EVAL_Z>(S, D, A, stream);
+    return cudaErrorInvalidValue;
+}
+
+} // namespace pht

@@ -269,3 +269,30 @@ def test_evaluate_vanishing_terms_huge_lifting(P):
     assert np.allclose(H[:, 0], np.exp(z[:, 0]), rtol=1e-14, atol=0)
     o = oracle.Oracle(sysm).evaluate(np.exp(z), np.exp(tau))
     assert np.allclose(H, o["H"], rtol=1e-14, atol=1e-300)
+
+
+@pytest.mark.parametrize("n,m,p", [(20, 50, 200), (12, 20, 97), (16, 30, 64)])
+def test_dense_tensor_core_evaluate(P, n, m, p):
+    """Config C4 (random dense Laurent system): the FP64 tensor-core (DMMA) evaluation path
+    (pht_dense.cuh) vs the oracle, scaled and unscaled, and against the generic path."""
+    sysm = W.random_dense(n, m, seed=n)
+    g = P.System.from_workload(sysm)
+    assert g.dense
+    x, t, _ = W.random_points(p, n, seed=5, rho_max=0.5)
+    o = oracle.Oracle(sysm).evaluate(x, t)
+    H, Jx, Jt, st = g.evaluate(_cuda(x), _cuda(t))
+    assert np.all(st.cpu().numpy() == 0)
+    assert eval_err(H.cpu().numpy(), o["H"], o["SH"]) <= 1e-10
+    assert eval_err(Jx.cpu().numpy(), o["Jx"], o["SJx"]) <= 1e-10
+    assert eval_err(Jt.cpu().numpy(), o["Jt"], o["SJt"]) <= 1e-10
+    Hs, Jxs, Jts, e2, _ = g.evaluate(_cuda(x), _cuda(t), scaled=True)
+    sc = np.exp2(e2.cpu().numpy().astype(float))
+    assert eval_err(Hs.cpu().numpy() * sc, o["H"], o["SH"]) <= 1e-10
+    z, tau = np.log(x), np.log(t)
+    Hl, Jz, Jtau, e2l, _ = g.evaluate_log(_cuda(z), _cuda(tau))
+    scl = np.exp2(e2l.cpu().numpy().astype(float))
+    assert eval_err(Jz.cpu().numpy() * scl[:, :, None], o["Jx"] * x[:, None, :], o["SJx"] * np.abs(x)[:, None, :]) <= 1e-10
+    # the direction solve for the same system runs on the generic kernel: still consistent
+    dE, dN, st2 = g.euler_newton(_cuda(x), _cuda(t))
+    be = backward_err(o["Jx"], dN.cpu().numpy(), -o["H"])
+    assert be[st2.cpu().numpy() == 0].max() <= 1e-10

@@ -66,6 +66,26 @@ __global__ void k_loglat(double *out, int iters)
     if (acc == 123.456) out[0] = acc;
 }
 
+// FP64 tensor core: mma.sync m8n8k4 f64 (lowers to DMMA on sm_100a), ILP independent accumulators
+template <int ILP>
+__global__ void k_dmma(double *out, int iters)
+{
+    double a = 1.0 + threadIdx.x * 1e-6, b = 0.5;
+    double c[ILP][2];
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < ILP; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) s += c[i][0] + c[i][1];
+    if (s == 123.456) out[0] = s;
+}
+
 int main()
 {
     double *d;
@@ -151,6 +171,20 @@ int main()
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         printf(", \"libdevice_log_atan2_G_per_s\": %.3f", iters * (double)blocks * threads / (ms * 1e-3) / 1e9);
+    }
+    {
+        const int iters = 20000, blocks = sms * 4, threads = 256;
+        k_dmma<4><<<blocks, threads>>>(d, 10);
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0);
+        k_dmma<4><<<blocks, threads>>>(d, iters);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        // each warp-level m8n8k4 = 8*8*4 = 256 FMAs = 512 flops
+        double flops = 512.0 * 4 * iters * (double)blocks * (threads / 32);
+        printf(", \"dmma_tflops\": %.3f", flops / (ms * 1e-3) / 1e12);
     }
     printf("}\n");
     return 0;
