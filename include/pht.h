@@ -83,8 +83,8 @@ int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *eq_offsets,
 void pht_system_destroy(pht_system *sys);
 
 /* Query: n, number of packed terms M, largest equation size, owning device. */
-#define PHT_SYS_DENSE 1 /* evaluation uses the FP64 tensor-core (DMMA) path: n >= 12 and at least
-                           half of the exponent entries nonzero (env PHT_DENSE=0/1 overrides) */
+#define PHT_SYS_DENSE 1 /* evaluation uses the FP64 tensor-core (DMMA) path: n >= 10 and no zero
+                           coefficient dropped (env PHT_DENSE=0/1 overrides) */
 int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative pht_status */
 
 int pht_system_info(const pht_system *sys, int32_t *n, int64_t *M, int32_t *max_terms,

@@ -151,13 +151,10 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
         pht_system_destroy(s);
         return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
     }
-    // dense policy: n >= 12 and at least half of the exponent entries nonzero (config C4),
-    // overridable with PHT_DENSE=0/1 (experiments)
+    // tensor-core evaluation policy: every system with n >= 10 (measured faster than the scalar
+    // kernel from n = 10 on, dense or sparse: profiles/r01_dense_tuning.txt); PHT_DENSE=0/1 overrides
     {
-        int64_t nnz = 0;
-        for (int64_t i = 0; i < M_in; ++i)
-            for (int j = 0; j < n; ++j) nnz += exps[i * n + j] != 0;
-        int want = (n >= 12 && n_dropped == 0 && 2 * nnz >= M_in * n) ? 1 : 0;
+        int want = (n >= 10 && n_dropped == 0) ? 1 : 0;
         if (const char *ev = getenv("PHT_DENSE")) want = (ev[0] == '1') && n_dropped == 0;
         if (want) {
             const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;

@@ -38,8 +38,14 @@ struct DGeo {
     static constexpr int KP = (N + 2 + 3) & ~3; // stage-2 K (vars + tau/const) padded to 4
     static constexpr int KS = KP / 4;          // stage-2 k-steps
     static constexpr int CT = (N + 2 + 7) / 8; // stage-4 column tiles of 8
-    static constexpr int NMT = 2;              // M-tiles (8 points) per warp
-    static constexpr int WARPS = 4;
+#ifndef PHT_DENSE_NMT
+#define PHT_DENSE_NMT 1
+#endif
+#ifndef PHT_DENSE_WARPS
+#define PHT_DENSE_WARPS 4
+#endif
+    static constexpr int NMT = PHT_DENSE_NMT;     // M-tiles (8 points) per warp
+    static constexpr int WARPS = PHT_DENSE_WARPS;
     static constexpr int PTS = WARPS * NMT * 8; // points per CTA
 };
 
@@ -62,7 +68,7 @@ struct DenseSmem {
 };
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 2) k_dense(const DevSys S, const DenseSys D, const Args A)
+__global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S, const DenseSys D, const Args A)
 {
     using G = DGeo<N>;
     constexpr int KP = G::KP, KS = G::KS, CT = G::CT, NMT = G::NMT, PTS = G::PTS;

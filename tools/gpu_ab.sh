@@ -1,3 +1,3 @@
-python -m pytest tests -m gpu -q -x 2>&1 | tail -12 > gpurun_out/gpu_tests.log
-python tools/eval_bench.py > gpurun_out/eval_bench.json 2> gpurun_out/eval_bench.err
-PHT_DENSE=1 python tools/eval_bench.py > gpurun_out/eval_bench_dense1.json 2> gpurun_out/eval_bench_dense1.err
+for v in lib_d1 lib_d1w8 lib_d1w2; do
+  PHT_LIB=$PWD/paper_2111_14317_b200/$v/libpht.so PHT_DENSE=1 python tools/eval_bench.py > gpurun_out/eb_$v.json 2>/dev/null
+done
