@@ -46,7 +46,8 @@ typedef enum {
     PHT_ERANGE = -5,       /* |exponent| > PHT_MAX_EXP or lifting < 0                    */
     PHT_ECUDA = -6,        /* a CUDA runtime call failed (see pht_last_cuda_error)        */
     PHT_ENOMEM = -7,       /* device or host allocation failed                           */
-    PHT_EUNSUPPORTED = -8  /* option not supported by this build                         */
+    PHT_EUNSUPPORTED = -8, /* option not supported by this build                         */
+    PHT_EJIT = -9          /* run-time compilation failed (NVRTC log: pht_last_cuda_error)  */
 } pht_status;
 
 /* per-point / per-path status bits */
@@ -85,7 +86,40 @@ void pht_system_destroy(pht_system *sys);
 /* Query: n, number of packed terms M, largest equation size, owning device. */
 #define PHT_SYS_DENSE 1 /* evaluation uses the FP64 tensor-core (DMMA) path: n >= 10 and no zero
                            coefficient dropped (env PHT_DENSE=0/1 overrides) */
+#define PHT_SYS_SPECIALIZED 2 /* system-specialised kernels loaded (pht_system_specialize) */
 int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative pht_status */
+
+/*
+ * System-specialised kernels: the one-time "Initialize" step of Alg. 1 extended to
+ * write the system's rows (a2-a4) as straight-line CUDA with the exponents,
+ * liftings and coefficients as literals, so that only the nonzero exponents are touched
+ * (nnz(A)/M = 1.6-5 on the benchmark systems vs n for the table-driven kernels), compiled at
+ * run time with NVRTC for sm_100a and loaded on the system's device.  Afterwards every entry
+ * point selected by `what` runs the specialised kernels on this handle; results agree with the
+ * generic kernels to rounding (same arithmetic per term, different summation order; rows keep
+ * the row_exp2 convention with the exponent taken from the row's largest term).
+ *   what   bit set of PHT_SPEC_* (0 = all): EVAL = pht_evaluate / pht_evaluate_log,
+ *          STEP = pht_euler_newton / pht_pc_step, TRACK = pht_track / pht_track_cells.
+ * Host-synchronous; compile time grows with the number of terms (about a second for the n = 10
+ * benchmark systems).  Calling it again with a subset of the compiled kernels is a no-op.
+ * Returns PHT_OK, PHT_EJIT (NVRTC failed: log in pht_last_cuda_error), PHT_ECUDA (load failed)
+ * or PHT_EINVAL.  Not thread-safe against concurrent calls on the same handle.
+ */
+#define PHT_SPEC_EVAL 1
+#define PHT_SPEC_STEP 2
+#define PHT_SPEC_TRACK 4
+#define PHT_SPEC_ALL 7
+int pht_system_specialize(pht_system *sys, int32_t what);
+
+/* Code-generator checks without a GPU (same inputs as pht_system_create, HOST pointers):
+ * pht_specialize_compile generates and compiles the specialised kernels (no load) and stores
+ * the cubin size; pht_specialize_source copies the generated CUDA source into buf (capacity
+ * cap, NUL-terminated, truncated) and returns the full length + 1, or a negative pht_status. */
+int pht_specialize_compile(int32_t n_eq, int32_t n_var, const int64_t *eq_offsets, const int32_t *exponents,
+                           const double *coeffs, const double *lifting, int32_t what, int64_t *cubin_bytes);
+int64_t pht_specialize_source(int32_t n_eq, int32_t n_var, const int64_t *eq_offsets,
+                              const int32_t *exponents, const double *coeffs, const double *lifting,
+                              char *buf, int64_t cap);
 
 int pht_system_info(const pht_system *sys, int32_t *n, int64_t *M, int32_t *max_terms,
                     int32_t *device);

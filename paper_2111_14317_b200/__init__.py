@@ -9,4 +9,4 @@ from ._lib import (PT_OK, PT_ZERO_COORD, PT_NONFINITE, PT_SINGULAR, PT_STEP_UNDE
 
 _load_lib()
 
-from .api import System, launch_count  # noqa: E402,F401
+from .api import System, launch_count, specialize_compile, specialize_source  # noqa: E402,F401

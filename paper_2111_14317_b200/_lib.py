@@ -16,6 +16,8 @@ LIB_PATH = os.environ.get("PHT_LIB") or os.path.join(_HERE, "lib", "libpht.so")
 PHT_MAX_N = 24
 PT_OK, PT_ZERO_COORD, PT_NONFINITE, PT_SINGULAR = 0, 1, 2, 4
 PT_STEP_UNDERFLOW, PT_MAX_STEPS, PT_DIVERGED = 8, 16, 32
+SYS_DENSE, SYS_SPECIALIZED = 1, 2
+SPEC_EVAL, SPEC_STEP, SPEC_TRACK, SPEC_ALL = 1, 2, 4, 7
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -35,6 +37,9 @@ SIGNATURES = {
     "pht_track_opts_default": (None, [ctypes.c_void_p]),
     "pht_track": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_track_cells": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "pht_system_specialize": (ctypes.c_int, [_vp, _i32]),
+    "pht_specialize_compile": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "pht_specialize_source": (_i64, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64]),
     "pht_launch_count": (_i64, []),
     "pht_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "pht_last_cuda_error": (ctypes.c_char_p, []),
@@ -77,6 +82,6 @@ def check(rc: int, what: str):
     if rc != 0:
         lib = load()
         msg = lib.pht_strerror(rc).decode()
-        if rc == -6:
+        if rc in (-6, -9):
             msg += ": " + lib.pht_last_cuda_error().decode()
         raise PhtError(f"{what} failed ({rc}): {msg}")

@@ -45,7 +45,16 @@ class System:
         check(lib.pht_system_info(h, ctypes.byref(nn), ctypes.byref(M), ctypes.byref(mt), ctypes.byref(dev)),
               "pht_system_info")
         self.n, self.M, self.max_terms = nn.value, M.value, mt.value
-        self.dense = bool(lib.pht_system_flags(h) & 1)  # FP64 tensor-core evaluation path
+        self.dense = bool(lib.pht_system_flags(h) & _lib.SYS_DENSE)  # FP64 tensor-core evaluation path
+
+    def specialize(self, what: int = _lib.SPEC_ALL):
+        """pht_system_specialize: compile and load the system-specialised kernels (NVRTC)."""
+        check(self._lib.pht_system_specialize(self._h, int(what)), "pht_system_specialize")
+        return self
+
+    @property
+    def specialized(self) -> bool:
+        return bool(self._lib.pht_system_flags(self._h) & _lib.SYS_SPECIALIZED)
 
     @classmethod
     def from_workload(cls, system, device: int = 0):
@@ -181,6 +190,40 @@ class System:
                                         _ptr(path_cell), ctypes.byref(o), _ptr(sv), _ptr(st), _stream(d)),
               "pht_track_cells")
         return st, sv
+
+
+def _host_tables(system):
+    off = np.ascontiguousarray(system.offsets, np.int64)
+    exps = np.ascontiguousarray(system.exps, np.int32)
+    c = np.ascontiguousarray(system.coeffs, np.complex128)
+    w = np.ascontiguousarray(system.lifting, np.float64)
+    return off, exps, c, w
+
+
+def specialize_source(system) -> str:
+    """The generated CUDA source of the specialised kernels (pht_specialize_source; no GPU)."""
+    lib = _lib.load()
+    off, exps, c, w = _host_tables(system)
+    args = (len(off) - 1, int(exps.shape[1]), off.ctypes.data_as(ctypes.c_void_p),
+            exps.ctypes.data_as(ctypes.c_void_p), c.ctypes.data_as(ctypes.c_void_p), w.ctypes.data_as(ctypes.c_void_p))
+    need = lib.pht_specialize_source(*args, None, 0)
+    check(int(need) if need < 0 else 0, "pht_specialize_source")
+    buf = ctypes.create_string_buffer(int(need))
+    lib.pht_specialize_source(*args, buf, int(need))
+    return buf.value.decode()
+
+
+def specialize_compile(system, what: int = _lib.SPEC_ALL) -> int:
+    """Generate + compile (NVRTC, sm_100a) the specialised kernels without loading them (no GPU);
+    returns the cubin size in bytes."""
+    lib = _lib.load()
+    off, exps, c, w = _host_tables(system)
+    nb = ctypes.c_int64()
+    check(lib.pht_specialize_compile(len(off) - 1, int(exps.shape[1]), off.ctypes.data_as(ctypes.c_void_p),
+                                     exps.ctypes.data_as(ctypes.c_void_p), c.ctypes.data_as(ctypes.c_void_p),
+                                     w.ctypes.data_as(ctypes.c_void_p), int(what), ctypes.byref(nb)),
+          "pht_specialize_compile")
+    return int(nb.value)
 
 
 def launch_count() -> int:

@@ -2,13 +2,16 @@
 // paper's Alg. 1 "Initialize") and the entry points that enqueue k_pht.
 #include "../../include/pht.h"
 #include "pht_dense.cuh"
+#include "pht_jit.h"
 #include "pht_kernels.cuh"
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <set>
 #include <string>
@@ -43,6 +46,12 @@ struct pht_system {
     int dense = 0;
     double *d_b2phi = nullptr, *d_b2th = nullptr, *d_b4 = nullptr;
     int *d_ntoff = nullptr;
+    // packed tables on the host (input of the code generator, pht_system_specialize)
+    std::vector<double> h_rec;
+    std::vector<int> h_off;
+    // system-specialised kernels (pht_jit.cu), or nullptr
+    std::mutex jit_mu;
+    pht::JitKernels *jit = nullptr;
     // workspace for the *_host entry points
     std::mutex ws_mu;
     int64_t ws_cap = 0;
@@ -73,11 +82,13 @@ struct DevGuard {
     }
 };
 
-extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
-                                 const double *coeffs, const double *lifting, int32_t device,
-                                 pht_system **out)
+// a0: validate, drop zero coefficients, pack per-term records
+//   [a_0 .. a_{n-1}, omega, log|c|, arg c, pad]   (DESIGN.md §2 "HBM/L1 layout")
+static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps, const double *coeffs,
+                       const double *lifting, std::vector<double> &rec, std::vector<int> &doff, int &max_terms,
+                       int64_t &M, int &n_dropped)
 {
-    if (!off || !exps || !coeffs || !lifting || !out) return PHT_EINVAL;
+    if (!off || !exps || !coeffs || !lifting) return PHT_EINVAL;
     if (n_eq != n_var || n_eq < 1 || n_eq > PHT_MAX_N) return PHT_ESHAPE;
     const int n = n_eq;
     if (off[0] != 0) return PHT_ESHAPE;
@@ -85,16 +96,13 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
         if (off[k + 1] < off[k]) return PHT_ESHAPE;
     const int64_t M_in = off[n];
     if (M_in >= (int64_t)1 << 30) return PHT_ESHAPE;
-
-    // a0: validate, drop zero coefficients, pack per-term records
-    //   [a_0 .. a_{n-1}, omega, log|c|, arg c, pad]   (DESIGN.md §2 "HBM/L1 layout")
     const int RS = pht::rec_stride(n);
-    std::vector<double> rec;
-    std::vector<int> doff(n + 1, 0);
-    int max_terms = 0;
+    rec.clear();
+    doff.assign(n + 1, 0);
+    max_terms = 0;
     rec.reserve((size_t)M_in * RS);
-    int64_t M = 0;
-    int n_dropped = 0;
+    M = 0;
+    n_dropped = 0;
     for (int k = 0; k < n; ++k) {
         std::set<std::vector<int32_t>> seen;
         int cnt = 0;
@@ -119,6 +127,21 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
         doff[k + 1] = (int)M;
         if (cnt > max_terms) max_terms = cnt;
     }
+    return PHT_OK;
+}
+
+extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
+                                 const double *coeffs, const double *lifting, int32_t device,
+                                 pht_system **out)
+{
+    if (!out) return PHT_EINVAL;
+    std::vector<double> rec;
+    std::vector<int> doff;
+    int max_terms = 0, n_dropped = 0;
+    int64_t M = 0;
+    const int prc = pack_system(n_eq, n_var, off, exps, coeffs, lifting, rec, doff, max_terms, M, n_dropped);
+    if (prc != PHT_OK) return prc;
+    const int n = n_eq;
 
     // exp / cis tables, rounded from 80-bit long double
     std::vector<double> etab(256), ctab(512);
@@ -138,6 +161,8 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     s->max_terms = max_terms;
     s->device = device;
     s->dropped = n_dropped;
+    s->h_rec = rec;
+    s->h_off = doff;
     cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device);
     cudaError_t e;
     if ((e = cudaMalloc(&s->d_rec, rec.size() * sizeof(double))) != cudaSuccess ||
@@ -230,6 +255,7 @@ extern "C" void pht_system_destroy(pht_system *s)
     cudaFree(s->d_b4);
     cudaFree(s->d_ntoff);
     cudaFree(s->ws);
+    pht::jit_free(s->jit);
     delete s;
 }
 
@@ -247,7 +273,94 @@ extern "C" int pht_system_info(const pht_system *s, int32_t *n, int64_t *M, int3
 extern "C" int pht_system_flags(const pht_system *s)
 {
     if (!s) return PHT_EINVAL;
-    return s->dense ? PHT_SYS_DENSE : 0;
+    int f = s->dense ? PHT_SYS_DENSE : 0;
+    if (s->jit) f |= PHT_SYS_SPECIALIZED;
+    return f;
+}
+
+// System-specialised kernels (pht_jit.cu): generate, compile (NVRTC, sm_100a), load.
+static thread_local std::string g_jit_log;
+
+extern "C" int pht_system_specialize(pht_system *s, int32_t what)
+{
+    if (!s) return PHT_EINVAL;
+    if (what == 0) what = PHT_SPEC_ALL;
+    if (what & ~PHT_SPEC_ALL) return PHT_EINVAL;
+    std::lock_guard<std::mutex> lk(s->jit_mu);
+    if (s->jit && (pht::jit_what(s->jit) & (unsigned)what) == (unsigned)what) return PHT_OK;
+    const std::string src = pht::jit_source(s->n, s->h_rec, s->h_off);
+    // process-wide cache of compiled images keyed by (generated source, kernel set): the same
+    // system loaded again (another device, another handle) is not recompiled
+    static std::mutex cache_mu;
+    static std::map<std::string, std::pair<std::vector<char>, std::vector<std::string>>> cache;
+    const std::string key = std::to_string(what) + "|" + src;
+    std::vector<char> cubin;
+    std::vector<std::string> names;
+    {
+        std::lock_guard<std::mutex> ck(cache_mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            cubin = it->second.first;
+            names = it->second.second;
+        }
+    }
+    if (cubin.empty()) {
+        if (pht::jit_compile(s->n, src, (unsigned)what, cubin, names, g_jit_log) != 0) {
+            g_cuda_err = "NVRTC: " + g_jit_log;
+            return PHT_EJIT;
+        }
+        std::lock_guard<std::mutex> ck(cache_mu);
+        cache[key] = {cubin, names};
+    }
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    cudaError_t e = cudaSuccess;
+    pht::JitKernels *J = pht::jit_load(s->n, (unsigned)what, cubin, names, &e);
+    if (!J) return cuda_fail(e);
+    pht::jit_free(s->jit);
+    s->jit = J;
+    return PHT_OK;
+}
+
+extern "C" int pht_specialize_compile(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
+                                      const double *coeffs, const double *lifting, int32_t what,
+                                      int64_t *cubin_bytes)
+{
+    std::vector<double> rec;
+    std::vector<int> doff;
+    int max_terms = 0, n_dropped = 0;
+    int64_t M = 0;
+    const int prc = pack_system(n_eq, n_var, off, exps, coeffs, lifting, rec, doff, max_terms, M, n_dropped);
+    if (prc != PHT_OK) return prc;
+    if (what == 0) what = PHT_SPEC_ALL;
+    if (what & ~PHT_SPEC_ALL) return PHT_EINVAL;
+    const std::string src = pht::jit_source(n_eq, rec, doff);
+    std::vector<char> cubin;
+    std::vector<std::string> names;
+    if (pht::jit_compile(n_eq, src, (unsigned)what, cubin, names, g_jit_log) != 0) {
+        g_cuda_err = "NVRTC: " + g_jit_log;
+        return PHT_EJIT;
+    }
+    if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
+    return PHT_OK;
+}
+
+extern "C" int64_t pht_specialize_source(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
+                                         const double *coeffs, const double *lifting, char *buf, int64_t cap)
+{
+    std::vector<double> rec;
+    std::vector<int> doff;
+    int max_terms = 0, n_dropped = 0;
+    int64_t M = 0;
+    const int prc = pack_system(n_eq, n_var, off, exps, coeffs, lifting, rec, doff, max_terms, M, n_dropped);
+    if (prc != PHT_OK) return prc;
+    const std::string src = pht::jit_source(n_eq, rec, doff);
+    if (buf && cap > 0) {
+        const size_t c = std::min((size_t)cap - 1, src.size());
+        memcpy(buf, src.data(), c);
+        buf[c] = 0;
+    }
+    return (int64_t)src.size() + 1;
 }
 
 static int dispatch(const pht_system *s, int mode, const pht::Args &A, void *stream)
@@ -258,7 +371,15 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A, void *str
     pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
-    const bool dense = s->dense && (mode == pht::MODE_EVAL_X || mode == pht::MODE_EVAL_Z);
+    const bool evalm = mode == pht::MODE_EVAL_X || mode == pht::MODE_EVAL_Z;
+    const unsigned need = evalm ? pht::JIT_EVAL : pht::JIT_STEP;
+    if (s->jit && (pht::jit_what(s->jit) & need)) {
+        e = pht::jit_launch(s->jit, mode, S, A, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return PHT_OK;
+    }
+    const bool dense = s->dense && evalm;
     const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff};
     switch (s->n) {
 #define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st); break;
@@ -430,7 +551,8 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
                          o.pred_log < 0 ? o.log_state : o.pred_log};
-    switch (s->n) {
+    if (s->jit && (pht::jit_what(s->jit) & pht::JIT_TRACK)) e = pht::jit_launch_track(s->jit, S, A, st, s->sms);
+    else switch (s->n) {
 #define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
         PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12) PHT_CASE(13) PHT_CASE(14)
@@ -476,6 +598,7 @@ extern "C" const char *pht_strerror(int code)
     case PHT_ECUDA: return "CUDA error";
     case PHT_ENOMEM: return "out of memory";
     case PHT_EUNSUPPORTED: return "unsupported";
+    case PHT_EJIT: return "run-time compilation of the specialised kernels failed (log: pht_last_cuda_error)";
     default: return "unknown error";
     }
 }

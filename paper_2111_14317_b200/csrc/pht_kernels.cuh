@@ -23,11 +23,20 @@
 //   a6  step        Euler prediction + K Newton iterations
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <atomic>
 #include <cstddef>
+#else
+// run-time compilation (pht_jit.cu, NVRTC): no host headers
+typedef unsigned char uint8_t;
+typedef long long int64_t;
+#ifndef INFINITY
+#define INFINITY __longlong_as_double(0x7ff0000000000000ll)
+#endif
+#endif
 
 namespace pht {
 
@@ -175,7 +184,7 @@ __device__ __forceinline__ double2 expcis(double y, double th, const double *eta
     // terms more than e^-2000 below the row scale flush to 0; clamping first keeps y*256/ln2
     // inside the 32-bit integer extracted from the shifter (|y| up to ~10^8 occurs for large
     // cell-shifted liftings)
-    y = fmax(y, -2000.0);
+    y = (y < -2000.0) ? -2000.0 : y; // (a select: cheaper than fmax, and NaN propagates)
     const double kf = fma(y, KC[0], SHIFT);
     const int ki = __double2loint(kf);
     const double kd = kf - SHIFT;
@@ -215,7 +224,7 @@ __device__ __forceinline__ double2 expcis(double y, double th, const double *eta
 // groups exactly fill the CTA's warps (no second round), and CTAs stay small (<= 8 warps) so
 // that two co-resident CTAs overlap each other's load / barrier phases.
 template <int N>
-struct Geo {
+struct GeoS {
     static constexpr int WL = N <= 5 ? 32 : (N <= 16 ? 16 : 8);
     static constexpr int NTW = N * WL;                 // W-layout threads
     static constexpr int NWARP = (NTW + 31) / 32;
@@ -230,6 +239,35 @@ struct Geo {
     // co-resident CTAs per SM: aim at 16 warps (4 per SMSP -> 128 registers per thread)
     static constexpr int MINB = N <= 12 ? (PHT_RT_SMEM(N) ? (16 / NWARP > 1 ? 16 / NWARP : 1) : 2) : 1;
 };
+
+// Geometry of the system-specialised kernels (pht_jit.cu): the generated row code is
+// straight-line per equation, so a warp must hold ONE equation for 32 points (W lanes = points,
+// warp = equation); the L-layout solve then covers PPW * N points per pass.
+#ifndef PHT_JIT_WARPS_PER_SM
+#define PHT_JIT_WARPS_PER_SM 20
+#endif
+template <int N>
+struct GeoJ {
+    static constexpr int WL = 32;
+    static constexpr int NTW = N * WL;
+    static constexpr int NWARP = N;
+    static constexpr int NT = NWARP * 32;
+    static constexpr int PPW = 32 / N;
+    static constexpr int PTS = PPW * N < 32 ? PPW * N : 32;
+    static constexpr int NGRP = (PTS + PPW - 1) / PPW;
+    static constexpr int RW = N + 2;
+    static constexpr int MS = (N * RW) | 1;
+    static constexpr int KS = (N + 3) & ~3;
+    static constexpr int MINB = PHT_JIT_WARPS_PER_SM / N > 1 ? (PHT_JIT_WARPS_PER_SM / N < 8 ? PHT_JIT_WARPS_PER_SM / N : 8) : 1;
+};
+
+#ifdef PHT_JIT
+template <int N>
+using Geo = GeoJ<N>;
+#else
+template <int N>
+using Geo = GeoS<N>;
+#endif
 
 template <int N>
 struct Smem {
@@ -378,6 +416,13 @@ struct RowAcc {
     }
 };
 
+#ifdef PHT_JIT
+// system-specialised rows: defined by the generated source (pht_jit.cu) after this header
+template <int N>
+__device__ void jit_row(const DevSys &S, const Smem<N> &sm, int k, int q, double2 (&row)[N + 2], int &e,
+                        const double *wq);
+#endif
+
 // a2-a4 for row k of point q: row = [G_1..G_N | G_tau | h] scaled by 2^-e.
 // Terms are processed two at a time (independent dependency chains for the FP64 pipe).
 // wq (optional): per-point lifting table (cell-shifted liftings omega', pht_track_cells); the
@@ -386,6 +431,10 @@ template <int N>
 __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int k, int q,
                                          double2 (&row)[N + 2], int &e, const double *wq = nullptr)
 {
+#ifdef PHT_JIT
+    jit_row<N>(S, sm, k, q, row, e, wq);
+    return;
+#endif
     constexpr int RS = rec_stride(N);
     PointLog<N, (bool)PHT_RT_SMEM(N)> pl;
     pl.template load<Smem<N>::WL>(sm.rt, q);
@@ -1017,6 +1066,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
     }
 }
 
+#ifndef __CUDACC_RTC__
 template <int N, bool LOGS>
 cudaError_t launch_track_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
@@ -1085,5 +1135,6 @@ cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream
     default: return cudaErrorInvalidValue;
     }
 }
+#endif // !__CUDACC_RTC__
 
 } // namespace pht

@@ -62,3 +62,24 @@ def test_package_import_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ImportError):
         _lib.load()
+
+
+def test_specialize_codegen_without_gpu():
+    """The code generator of pht_system_specialize (one straight-line row per equation, only the
+    nonzero exponents touched) and its NVRTC compile for sm_100a run without a GPU."""
+    import paper_2111_14317_b200 as P
+    import workloads as W
+    # cyclic-3: f1 = x1 + x2 + x3, f2 = x1x2 + x2x3 + x3x1, f3 = x1x2x3 - 1
+    sysm = W.cyclic(3, lift_max=10)
+    src = P.specialize_source(sysm)
+    assert "jit_row<3>" in src and src.count("case ") == 3
+    # 8 terms -> 8 exp*cis evaluations; the constant term of f3 has no variable in phi
+    assert src.count("PHT_EXPCIS((p") == sysm.offsets[-1] == 8
+    body3 = src[src.index("case 2:"):src.index("default:")]
+    assert "(v0.x + v1.x) + v2.x" in body3 or "((v0.x + v1.x) + v2.x)" in body3
+    # the G_j updates touch exactly the nonzero exponents: nnz(A) = 3 + 6 + 3 = 12 complex updates
+    assert src.count(".x += w.x;") - src.count("h.x += w.x;") == 12
+    nb = P.specialize_compile(sysm, P._lib.SPEC_STEP)
+    assert nb > 0
+    with pytest.raises(P.PhtError):
+        P.specialize_compile(sysm, 64)

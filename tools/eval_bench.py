@@ -1,5 +1,6 @@
 """Standalone pht_evaluate throughput on several configs (device-resident, CUDA events)."""
 import json
+import time
 import os
 import sys
 
@@ -14,6 +15,8 @@ for name, sysm, p in [("cyclic-5", W.cyclic(5), 1 << 22), ("cyclic-10", W.cyclic
                       ("katsura-10", W.katsura(10, lift_max=100), 1 << 21), ("noon-10", W.noon(10, lift_max=100), 1 << 21),
                       ("random-20x50", W.random_dense(20, 50), 1 << 18)]:
     g = P.System.from_workload(sysm)
+    if os.environ.get("PHT_SPEC") == "1" and sysm.offsets[-1] <= 256:
+        t1 = time.time(); g.specialize(); print(json.dumps({"specialize_s": time.time() - t1}), file=sys.stderr)
     x, t, _ = W.random_points(p, sysm.n, seed=1, rho_max=0.5 if sysm.n > 12 else 1.0)
     xd, td = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()
     for _ in range(3):

@@ -32,6 +32,8 @@ for item in which:
         z, tau0, ids = SS.start_points_from_cells(sysm, cells)
     prep = time.time() - t0
     g = P.System.from_workload(sysm)
+    if os.environ.get("PHT_SPEC") == "1" and sysm.offsets[-1] <= 256:
+        t1 = time.time(); g.specialize(); print(json.dumps({"specialize_s": time.time() - t1}), file=sys.stderr)
     out = {}
     for rep in range(2):
         zd, td = torch.from_numpy(z.copy()).cuda(), torch.from_numpy(tau0.copy()).cuda()
