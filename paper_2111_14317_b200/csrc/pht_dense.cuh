@@ -58,8 +58,8 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 
 template <int N>
 struct DenseSmem {
-    double exptab[256];
-    double2 cistab[256];
+    double exptab[TAB_E];
+    double2 cistab[TAB_C];
     double ap[DGeo<N>::PTS][DGeo<N>::KP + 1]; // A operand rows for phi: rho_j, tau, 1
     double at[DGeo<N>::PTS][DGeo<N>::KP + 1]; // A operand rows for theta: theta_j, 0, 1
     double2 inv[DGeo<N>::PTS][N + 1];         // 1/x (EVAL_X)
@@ -76,10 +76,7 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
     DenseSmem<N> &sm = *reinterpret_cast<DenseSmem<N> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, r = lane & 3; // fragment coordinates
-    for (int i = tid; i < 256; i += G::WARPS * 32) {
-        sm.exptab[i] = __ldg(S.exptab + i);
-        sm.cistab[i] = __ldg(S.cistab + i);
-    }
+    load_tables(S, sm.exptab, sm.cistab, tid, G::WARPS * 32);
     const int64_t base = (int64_t)blockIdx.x * PTS;
     for (int q = tid; q < PTS; q += G::WARPS * 32) sm.st[q] = 0;
     __syncthreads();

@@ -106,8 +106,45 @@ __device__ constexpr double INV_2PI = 0x1.45f306dc9c883p-3;
 __device__ constexpr double TWO_PI_HI = 0x1.921fb54400000p+2;
 __device__ constexpr double TWO_PI_LO = 0x1.0b4611a626331p-32;
 
+// exp / cis tables in shared memory.  Default: 256 entries (2^(j/256), cis(2 pi j/256)), one copy;
+// the data-dependent lookups of a warp cause bank conflicts (ncu: ~60% excess wavefronts on these
+// two loads).  PHT_TAB64=1: 64 entries replicated per bank (16 copies of 2^(j/64), 8 copies of
+// cis(2 pi j/64), copy = lane mod 16 / mod 8: conflict free) at one more polynomial term per
+// function -- measured 3% slower on the step (profiles/r01_tables.txt), so off.
+#ifndef PHT_TAB64
+#define PHT_TAB64 0
+#endif
+#if PHT_TAB64
+constexpr int TAB_E = 64 * 16, TAB_C = 64 * 8;
+#else
+constexpr int TAB_E = 256, TAB_C = 256;
+#endif
+
 // Polynomial / reduction constants as a __constant__ table: the compiler then feeds them to DFMA
 // as constant-bank operands instead of materialising each 64-bit immediate with two UMOVs.
+#if PHT_TAB64
+__constant__ double KC[20] = {
+    0x1.71547652b82fep+6,  // 0 64/ln2
+    0x1.62e42fee00000p-7,  // 1 ln2/64 hi
+    0x1.a39ef35793c76p-39, // 2 ln2/64 lo
+    1.0 / 24.0,            // 3
+    1.0 / 6.0,             // 4
+    0x1.45f306dc9c883p+3,  // 5 64/(2pi)
+    0x1.921fb54400000p-4,  // 6 2pi/64 in three parts
+    0x1.0b4611a600000p-38, // 7
+    0x1.3198a2e037073p-73, // 8
+    1.0 / 120.0,           // 9
+    -1.0 / 6.0,            // 10
+    -1.0 / 720.0,          // 11
+    0x1.62e42fee00000p-1,  // 12 ln2 hi
+    0x1.a39ef35793c76p-33, // 13 ln2 lo
+    0x1.71547652b82fep+0,  // 14 1/ln2
+    0.0,                   // 15
+    -1.0 / 5040.0,         // 16
+    1.0 / 40320.0,         // 17
+    1.0 / 120.0,           // 18
+    0.0};
+#else
 __constant__ double KC[16] = {
     0x1.71547652b82fep+8,  // 0 256/ln2
     0x1.62e42fee00000p-9,  // 1 ln2/256 hi
@@ -125,6 +162,7 @@ __constant__ double KC[16] = {
     0x1.a39ef35793c76p-33, // 13 ln2 lo
     0x1.71547652b82fep+0,  // 14 1/ln2
     0.0};
+#endif
 
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
@@ -146,6 +184,20 @@ __device__ __forceinline__ double2 crecip(double2 b)
         double r = b.x / b.y, d = 1.0 / fma(b.x, r, b.y);
         return make_double2(r * d, -d);
     }
+}
+
+// exp / cis tables -> shared memory (layout: see PHT_TAB64); S holds the 256-entry tables
+__device__ __forceinline__ void load_tables(const DevSys &S, double *et, double2 *ct, int tid, int nt)
+{
+#if PHT_TAB64
+    for (int i = tid; i < TAB_E; i += nt) et[i] = __ldg(S.exptab + ((i >> 4) << 2));
+    for (int i = tid; i < TAB_C; i += nt) ct[i] = __ldg(S.cistab + ((i >> 3) << 2));
+#else
+    for (int i = tid; i < 256; i += nt) {
+        et[i] = __ldg(S.exptab + i);
+        ct[i] = __ldg(S.cistab + i);
+    }
+#endif
 }
 
 // a1: rho = log|x|, vartheta = arg x (principal branch, ledger R15), 1/x.
@@ -179,12 +231,39 @@ __device__ __forceinline__ void log_split(double2 x, double &rho, double &th, do
 // a3: w = exp(y) * (cos th + i sin th), y <= ~0.35 by construction of the row exponent.
 // Table-driven: 2^(j/256) and cis(2 pi j/256) in shared memory, degree-4/5/6 polynomials on
 // the reduced arguments (|r| <= ln2/512, |s| <= pi/256); error <= ~4 ulp.
+// PHT_TAB64=1: 64-entry bank-replicated tables, degree 5/7/8 (|r| <= ln2/128, |s| <= pi/64).
 __device__ __forceinline__ double2 expcis(double y, double th, const double *etab, const double2 *ctab)
 {
     // terms more than e^-2000 below the row scale flush to 0; clamping first keeps y*256/ln2
     // inside the 32-bit integer extracted from the shifter (|y| up to ~10^8 occurs for large
     // cell-shifted liftings)
     y = (y < -2000.0) ? -2000.0 : y; // (a select: cheaper than fmax, and NaN propagates)
+#if PHT_TAB64
+    unsigned lane;
+    asm("mov.u32 %0, %%laneid;" : "=r"(lane));
+    // |r| <= ln2/128: e^r to r^5 (truncation 3.5e-17); |s| <= pi/64: sin to s^7, cos to s^8
+    const double kf = fma(y, KC[0], SHIFT);
+    const int ki = __double2loint(kf);
+    const double kd = kf - SHIFT;
+    double r = fma(kd, -KC[1], y);
+    r = fma(kd, -KC[2], r);
+    const double p = fma(fma(fma(fma(fma(r, KC[18], KC[3]), r, KC[4]), r, 0.5), r, 1.0), r, 1.0);
+    double mag = etab[((ki & 63) << 4) | (lane & 15)] * p;
+    const int m = ki >> 6;
+    const unsigned hi = (unsigned)__double2hiint(mag) + ((unsigned)m << 20);
+    mag = (m < -1000) ? 0.0 : __hiloint2double((int)hi, __double2loint(mag));
+
+    const double qf = fma(th, KC[5], SHIFT);
+    const int qi = __double2loint(qf);
+    const double qd = qf - SHIFT;
+    double s = fma(qd, -KC[6], th);
+    s = fma(qd, -KC[7], s);
+    s = fma(qd, -KC[8], s);
+    const double s2 = s * s;
+    const double sn = fma(s * s2, fma(s2, fma(s2, KC[16], KC[9]), KC[10]), s);
+    const double cs = fma(s2, fma(s2, fma(s2, fma(s2, KC[17], KC[11]), KC[3]), -0.5), 1.0);
+    const double2 T = ctab[((qi & 63) << 3) | (lane & 7)];
+#else
     const double kf = fma(y, KC[0], SHIFT);
     const int ki = __double2loint(kf);
     const double kd = kf - SHIFT;
@@ -206,6 +285,7 @@ __device__ __forceinline__ double2 expcis(double y, double th, const double *eta
     const double sn = fma(s * s2, fma(s2, KC[9], KC[10]), s);
     const double cs = fma(s2, fma(s2, fma(s2, KC[11], KC[3]), -0.5), 1.0);
     const double2 T = ctab[qi & 255];
+#endif
     const double cr = fma(T.x, cs, -T.y * sn);
     const double ci = fma(T.y, cs, T.x * sn);
     return make_double2(mag * cr, mag * ci);
@@ -274,8 +354,8 @@ struct Smem {
     // [variable][point] tiles use a row stride of WL + 1 (odd in 16-byte units): accesses with
     // consecutive threads on consecutive variables of a point are then bank-conflict free.
     static constexpr int WL = Geo<N>::WL + 1;
-    double exptab[256];
-    double2 cistab[256];
+    double exptab[TAB_E];
+    double2 cistab[TAB_C];
     double2 rt[N][WL];    // (rho, vartheta) per variable
     double2 xs[N][WL];    // x (or z) of the tile
     double2 inv[N][WL];   // 1/x (EVAL_X); staging of dE (DIRS)
@@ -629,10 +709,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
     const int tid = threadIdx.x;
     const int k = tid / WL, q = tid % WL;           // W layout
     const int lane = tid & 31, warp = tid >> 5;      // L layout
-    for (int i = tid; i < 256; i += G::NT) {
-        sm.exptab[i] = __ldg(S.exptab + i);
-        sm.cistab[i] = __ldg(S.cistab + i);
-    }
+    load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
     const int64_t base = (int64_t)blockIdx.x * PTS;
     const int64_t gq = base + q;
     const bool valid = (k < N) && (q < PTS) && (gq < A.P);
@@ -907,10 +984,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
     const int k = tid / WL, q = tid % WL;
     const int lane = tid & 31, warp = tid >> 5;
     const TrackOpts &o = A.o;
-    for (int i = tid; i < 256; i += G::NT) {
-        sm.exptab[i] = __ldg(S.exptab + i);
-        sm.cistab[i] = __ldg(S.cistab + i);
-    }
+    load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
     if (tid < WL) {
         T.done_path[tid] = -1;
         T.cell[tid] = 0;
