@@ -177,7 +177,10 @@ int pht_pc_step(const pht_system *sys, int64_t p, double *x, double *tau, const 
 /*
  * pht_pc_step on HOST buffers (end-to-end entry point): copies x, tau, dtau to a device
  * workspace owned by the handle, runs the step, copies x, tau, status, dn_norm back and
- * synchronises.  Host pointers may be pageable or pinned.  Serialised per handle.
+ * synchronises.  Pipelined (P:807-824 batch pipelining): the points are cut into chunks that
+ * run copy-in -> step -> copy-out on three internal streams ordered after `stream`, so copies in
+ * both directions overlap the kernels (requires pinned host memory; pageable memory works but
+ * does not overlap).  Results are identical to pht_pc_step.  Serialised per handle.
  */
 int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
                      const double *dtau, int32_t newton_iters, uint8_t *status,

@@ -135,11 +135,13 @@ class System:
                                     _ptr(dn), _stream(d)), "pht_pc_step")
         return st, dn
 
-    def pc_step_host(self, x: np.ndarray, tau: np.ndarray, dtau: np.ndarray, newton_iters: int = 1):
-        """pht_pc_step_host on host numpy buffers (x, tau updated in place)."""
+    def pc_step_host(self, x: np.ndarray, tau: np.ndarray, dtau: np.ndarray, newton_iters: int = 1,
+                     status: np.ndarray = None, dn_norm: np.ndarray = None):
+        """pht_pc_step_host on host numpy buffers (x, tau updated in place; pass pinned buffers,
+        including status/dn_norm, for copy/compute overlap)."""
         p = x.shape[0]
-        st = np.empty(p, np.uint8)
-        dn = np.empty(p, np.float64)
+        st = status if status is not None else np.empty(p, np.uint8)
+        dn = dn_norm if dn_norm is not None else np.empty(p, np.float64)
         d = self._dev()
         check(self._lib.pht_pc_step_host(self._h, p, x.ctypes.data_as(ctypes.c_void_p),
                                          tau.ctypes.data_as(ctypes.c_void_p), dtau.ctypes.data_as(ctypes.c_void_p),

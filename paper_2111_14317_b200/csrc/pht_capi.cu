@@ -52,8 +52,11 @@ struct pht_system {
     // system-specialised kernels (pht_jit.cu), or nullptr
     std::mutex jit_mu;
     pht::JitKernels *jit = nullptr;
-    // workspace for the *_host entry points
+    // workspace and copy/compute streams of the *_host entry points
     std::mutex ws_mu;
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t hev0 = nullptr;
     int64_t ws_cap = 0;
     void *ws = nullptr;
 };
@@ -255,6 +258,11 @@ extern "C" void pht_system_destroy(pht_system *s)
     cudaFree(s->d_b4);
     cudaFree(s->d_ntoff);
     cudaFree(s->ws);
+    for (int u = 0; u < 3; ++u) {
+        if (s->hs[u]) cudaStreamDestroy(s->hs[u]);
+        if (s->hev[u]) cudaEventDestroy(s->hev[u]);
+    }
+    if (s->hev0) cudaEventDestroy(s->hev0);
     pht::jit_free(s->jit);
     delete s;
 }
@@ -456,6 +464,23 @@ extern "C" int pht_pc_step(const pht_system *s, int64_t p, double *x, double *ta
     return dispatch(s, pht::MODE_STEP, A, stream);
 }
 
+// Host-buffer step, pipelined (the batch pipelining of P:807-824 as stream
+// overlap): the points are cut into chunks; chunk c runs H2D -> step kernel -> D2H on internal
+// stream c mod PHT_HOST_STREAMS, so the two copy directions and the kernels of different chunks
+// overlap (copy engines and SMs work concurrently; pinned host memory needed for overlap).
+#define PHT_HOST_STREAMS 3
+static int ensure_streams(pht_system *s)
+{
+    if (s->hs[0]) return PHT_OK;
+    for (int u = 0; u < PHT_HOST_STREAMS; ++u) {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->hs[u], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->hev[u], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    cudaError_t e = cudaEventCreateWithFlags(&s->hev0, cudaEventDisableTiming);
+    return e == cudaSuccess ? PHT_OK : cuda_fail(e);
+}
+
 extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, double *tau, const double *dtau,
                                 int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
 {
@@ -476,23 +501,43 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
         if ((e = cudaMalloc(&s->ws, need)) != cudaSuccess) return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
         s->ws_cap = (int64_t)need;
     }
+    int rc = ensure_streams(s);
+    if (rc != PHT_OK) return rc;
     char *w = (char *)s->ws;
     double *dx = (double *)w, *dtu = (double *)(w + bx), *ddt = (double *)(w + bx + bt),
            *ddn = (double *)(w + bx + 2 * bt);
     uint8_t *dst = (uint8_t *)(w + bx + 3 * bt);
     cudaStream_t st = (cudaStream_t)stream;
-    if ((e = cudaMemcpyAsync(dx, x, bx, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dtu, tau, bt, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(ddt, dtau, bt, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-        return cuda_fail(e);
-    int rc = pht_pc_step(s, p, dx, dtu, ddt, newton_iters, dst, ddn, stream);
-    if (rc != PHT_OK) return rc;
-    if ((e = cudaMemcpyAsync(x, dx, bx, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(tau, dtu, bt, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (status && (e = cudaMemcpyAsync(status, dst, bs, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
-        (dn_norm && (e = cudaMemcpyAsync(dn_norm, ddn, bt, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
-        (e = cudaStreamSynchronize(st)) != cudaSuccess)
-        return cuda_fail(e);
+    // the caller's stream orders us after its earlier work; we order it after our copies
+    if ((e = cudaEventRecord(s->hev0, st)) != cudaSuccess) return cuda_fail(e);
+    for (int u = 0; u < PHT_HOST_STREAMS; ++u)
+        if ((e = cudaStreamWaitEvent(s->hs[u], s->hev0, 0)) != cudaSuccess) return cuda_fail(e);
+    // chunks: ~1/8 of the batch, at least 32K points (launch + copy latency stay amortised)
+    int64_t chunk = (p + 7) / 8;
+    if (chunk < 32768) chunk = 32768;
+    int c = 0;
+    for (int64_t b = 0; b < p; b += chunk, ++c) {
+        const int64_t m = (p - b < chunk) ? p - b : chunk;
+        cudaStream_t cs_ = s->hs[c % PHT_HOST_STREAMS];
+        const size_t ox = (size_t)b * n * 2, mx = (size_t)m * n * 16, mt = (size_t)m * 8;
+        if ((e = cudaMemcpyAsync(dx + ox, x + ox, mx, cudaMemcpyHostToDevice, cs_)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dtu + b, tau + b, mt, cudaMemcpyHostToDevice, cs_)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(ddt + b, dtau + b, mt, cudaMemcpyHostToDevice, cs_)) != cudaSuccess)
+            return cuda_fail(e);
+        rc = pht_pc_step(s, m, dx + ox, dtu + b, ddt + b, newton_iters, dst + b, ddn + b, (void *)cs_);
+        if (rc != PHT_OK) return rc;
+        if ((e = cudaMemcpyAsync(x + ox, dx + ox, mx, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(tau + b, dtu + b, mt, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess ||
+            (status && (e = cudaMemcpyAsync(status + b, dst + b, (size_t)m, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess) ||
+            (dn_norm && (e = cudaMemcpyAsync(dn_norm + b, ddn + b, mt, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess))
+            return cuda_fail(e);
+    }
+    for (int u = 0; u < PHT_HOST_STREAMS && u < c; ++u) {
+        if ((e = cudaEventRecord(s->hev[u], s->hs[u])) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(st, s->hev[u], 0)) != cudaSuccess)
+            return cuda_fail(e);
+    }
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
     return PHT_OK;
 }
 

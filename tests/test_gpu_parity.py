@@ -218,16 +218,23 @@ def test_pc_step_parity(P, name, p, K):
     assert np.allclose(dn[well], dno[well], rtol=1e-6, atol=1e-12)
 
 
-def test_pc_step_host_equals_device(P):
+@pytest.mark.parametrize("p", [500, 100_003])
+def test_pc_step_host_equals_device(P, p):
+    """The pipelined host-buffer entry point (chunks on 3 streams; 100,003 points = 4 chunks with
+    a ragged last one) gives bitwise the device entry point's results, pinned or pageable."""
     sysm = W.cyclic(10, lift_max=100)
     g = P.System.from_workload(sysm)
-    x, _, tau = W.random_points(500, 10, seed=13)
-    dtau = np.full(500, 0.02)
+    x, _, tau = W.random_points(p, 10, seed=13)
+    dtau = np.full(p, 0.02)
     xd, td = _cuda(x), _cuda(tau)
     g.pc_step(xd, td, _cuda(dtau))
     xh, th = x.copy(), tau.copy()
     g.pc_step_host(xh, th, dtau)
     assert np.array_equal(xh, xd.cpu().numpy()) and np.array_equal(th, td.cpu().numpy())
+    xp = torch.from_numpy(x.copy()).pin_memory()
+    tp = torch.from_numpy(tau.copy()).pin_memory()
+    g.pc_step_host(xp.numpy(), tp.numpy(), dtau)
+    assert np.array_equal(xp.numpy(), xh) and np.array_equal(tp.numpy(), th)
 
 
 @pytest.mark.parametrize("name,n", [("cyclic-5", 5), ("noon-5", 5), ("cyclic-10", 10)])
