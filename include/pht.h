@@ -125,6 +125,22 @@ int pht_system_info(const pht_system *sys, int32_t *n, int64_t *M, int32_t *max_
                     int32_t *device);
 
 /*
+ * Direction solver used by pht_euler_newton, pht_pc_step(_host), pht_track(_cells) on this
+ * handle (a5; both solve G [dE | dN] = -[G_tau | h] in log coordinates):
+ *   PHT_SOLVER_LU (default)  Gauss-Jordan with partial pivoting, one warp-lane per matrix row
+ *                            (the consolidated 2-RHS elimination of BASELINE.json north_star).
+ *   PHT_SOLVER_QR            the paper's own mechanism (Alg. 3):
+ *                            Householder QR (no pivoting, backward stable), one lane per column,
+ *                            the right-hand sides carried through Q^H, then back substitution.
+ *                            Singular: |R_kk| <= 1e-14 ||G||_F (reading R26).  About twice the
+ *                            cost of LU; a robustness path for ill-conditioned Jx.
+ * Not synchronised with calls in flight on the handle.  Returns PHT_OK or PHT_EINVAL.
+ */
+#define PHT_SOLVER_LU 0
+#define PHT_SOLVER_QR 1
+int pht_system_set_solver(pht_system *sys, int32_t solver);
+
+/*
  * Batched evaluation of H, dH/dx, dH/dt (§5, Alg. 2).
  *   p         number of points (>= 0; 0 is a no-op).
  *   x         c128[p][n] points in (C*)^n.

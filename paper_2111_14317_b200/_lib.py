@@ -18,6 +18,7 @@ PT_OK, PT_ZERO_COORD, PT_NONFINITE, PT_SINGULAR = 0, 1, 2, 4
 PT_STEP_UNDERFLOW, PT_MAX_STEPS, PT_DIVERGED = 8, 16, 32
 SYS_DENSE, SYS_SPECIALIZED = 1, 2
 SPEC_EVAL, SPEC_STEP, SPEC_TRACK, SPEC_ALL = 1, 2, 4, 7
+SOLVER_LU, SOLVER_QR = 0, 1
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -37,6 +38,7 @@ SIGNATURES = {
     "pht_track_opts_default": (None, [ctypes.c_void_p]),
     "pht_track": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_track_cells": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "pht_system_set_solver": (ctypes.c_int, [_vp, _i32]),
     "pht_system_specialize": (ctypes.c_int, [_vp, _i32]),
     "pht_specialize_compile": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
     "pht_specialize_source": (_i64, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64]),

@@ -47,6 +47,12 @@ class System:
         self.n, self.M, self.max_terms = nn.value, M.value, mt.value
         self.dense = bool(lib.pht_system_flags(h) & _lib.SYS_DENSE)  # FP64 tensor-core evaluation path
 
+    def set_solver(self, solver: str = "lu"):
+        """pht_system_set_solver: 'lu' (Gauss-Jordan, default) or 'qr' (Householder, P:708-726)."""
+        code = {"lu": _lib.SOLVER_LU, "qr": _lib.SOLVER_QR}[solver]
+        check(self._lib.pht_system_set_solver(self._h, code), "pht_system_set_solver")
+        return self
+
     def specialize(self, what: int = _lib.SPEC_ALL):
         """pht_system_specialize: compile and load the system-specialised kernels (NVRTC)."""
         check(self._lib.pht_system_specialize(self._h, int(what)), "pht_system_specialize")

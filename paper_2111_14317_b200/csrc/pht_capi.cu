@@ -38,6 +38,7 @@ struct pht_system {
     int device = 0;
     int sms = 148;
     int dropped = 0; // terms with c = 0 removed by the packer
+    int solver = 0;  // PHT_SOLVER_LU / PHT_SOLVER_QR (pht_system_set_solver)
     double2 *d_rec = nullptr;
     int *d_off = nullptr;
     double *d_exptab = nullptr;
@@ -286,6 +287,13 @@ extern "C" int pht_system_flags(const pht_system *s)
     return f;
 }
 
+extern "C" int pht_system_set_solver(pht_system *s, int32_t solver)
+{
+    if (!s || (solver != PHT_SOLVER_LU && solver != PHT_SOLVER_QR)) return PHT_EINVAL;
+    s->solver = solver;
+    return PHT_OK;
+}
+
 // System-specialised kernels (pht_jit.cu): generate, compile (NVRTC, sm_100a), load.
 static thread_local std::string g_jit_log;
 
@@ -371,14 +379,16 @@ extern "C" int64_t pht_specialize_source(int32_t n_eq, int32_t n_var, const int6
     return (int64_t)src.size() + 1;
 }
 
-static int dispatch(const pht_system *s, int mode, const pht::Args &A, void *stream)
+static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *stream)
 {
-    if (A.P == 0) return PHT_OK;
+    if (A0.P == 0) return PHT_OK;
     DevGuard g(s->device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
     pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
+    pht::Args A = A0;
+    A.solver = s->solver;
     const bool evalm = mode == pht::MODE_EVAL_X || mode == pht::MODE_EVAL_Z;
     const unsigned need = evalm ? pht::JIT_EVAL : pht::JIT_STEP;
     if (s->jit && (pht::jit_what(s->jit) & need)) {
@@ -593,6 +603,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     A.path_cell = path_cell;
     A.ncells = (int)ncells;
     A.M = (int)s->M;
+    A.solver = s->solver;
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
                          o.pred_log < 0 ? o.log_state : o.pred_log};

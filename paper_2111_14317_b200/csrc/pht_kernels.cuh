@@ -44,6 +44,8 @@ enum Mode : int { MODE_EVAL_X = 0, MODE_EVAL_Z = 1, MODE_DIRS = 2, MODE_STEP = 3
 
 enum : int { PT_ZERO_COORD = 1, PT_NONFINITE = 2, PT_SINGULAR = 4 };
 
+enum : int { SOLVER_LU = 0, SOLVER_QR = 1 };
+
 // Term record stride in doubles: a_0..a_{n-1}, omega, log|c|, arg c, padded to even.
 __host__ __device__ constexpr int rec_stride(int n) { return (n + 3 + 1) & ~1; }
 
@@ -68,6 +70,7 @@ struct Args {
     const double *dtau;  // STEP
     double *dnnorm;      // STEP
     int K;               // STEP: Newton iterations
+    int solver;          // DIRS/STEP: SOLVER_LU (Gauss-Jordan, lsolve) or SOLVER_QR (qsolve)
 };
 
 // Tracker options (include/pht.h pht_track_opts) and arguments.
@@ -87,6 +90,7 @@ struct TrackArgs {
     const double *cellw;       // optional [ncells][M] cell-shifted liftings (pht_track_cells)
     const int *path_cell;      // [P] cell of each path
     int ncells, M;
+    int solver; // SOLVER_LU / SOLVER_QR
     TrackOpts o;
 };
 
@@ -699,6 +703,122 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
     dN = make_double2(-n.x, -n.y);
 }
 
+// a5, QR route (the paper's mechanism P:708-726, Alg. 3).
+// Column layout: lane (seg, c) of a warp holds COLUMN c of [G | G_tau | h] of point
+// q = g*PPQ + seg (PPQ = 32 / (N+2) points per warp).  Householder reflections from the left
+// (no pivoting: backward stable for any Jx) reduce G to R and carry the two right-hand-side
+// columns along (lanes N, N+1 end with Q^H G_tau, Q^H h); a row-oriented back substitution
+// R [dE | dN] = -Q^H [G_tau | h] then leaves dE_c, dN_c on lane c.  The reflector of step k is
+// built by lane k from its column and published through the point's matrix slot.  Singular
+// (reading R26): |R_kk| <= 1e-14 ||G||_F or non-finite.  inv/out2 of the point serve as the
+// broadcast buffer of the back substitution.
+template <int N>
+__device__ __forceinline__ void qsolve(Smem<N> &sm, int lane, int g, int &col, double2 &dE, double2 &dN,
+                                       bool &singular, bool &act, int &q)
+{
+    constexpr int RW = Geo<N>::RW, MS = Geo<N>::MS, PPQ = 32 / RW;
+    const int seg0 = lane / RW;
+    const bool inseg = seg0 < PPQ;
+    const int seg = inseg ? seg0 : 0, c = inseg ? lane - seg0 * RW : 0;
+    q = g * PPQ + seg;
+    const bool live = inseg && (q < Geo<N>::PTS);
+    act = live && (c < N);
+    const int qc = live ? q : 0;
+    double2 *slot = sm.mat + qc * MS;
+    double *scr = reinterpret_cast<double *>(slot);
+    double2 a[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) a[r] = slot[r * RW + c];
+    double n2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < N; ++r) n2 = fma(a[r].x, a[r].x, fma(a[r].y, a[r].y, n2));
+    __syncwarp();
+    if (live && c < N) scr[c] = n2;
+    __syncwarp();
+    double fro2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < N; ++u) fro2 += scr[u];
+    __syncwarp();
+    const double thr = 1e-14 * sqrt(fro2);
+    singular = !isfinite(thr);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        // reflector from column k (every lane evaluates it for its own column; lane k publishes)
+        double s2 = 0.0;
+#pragma unroll
+        for (int r = k; r < N; ++r) s2 = fma(a[r].x, a[r].x, fma(a[r].y, a[r].y, s2));
+        const double nrm = sqrt(s2), ax0 = sqrt(fma(a[k].x, a[k].x, a[k].y * a[k].y));
+        const double2 ph = (ax0 > 0.0) ? make_double2(a[k].x / ax0, a[k].y / ax0) : make_double2(1.0, 0.0);
+        const double2 alpha = make_double2(-ph.x * nrm, -ph.y * nrm);
+        if (live && c == k) {
+            const double den = nrm * (nrm + ax0);
+            scr[2 * N] = (den > 0.0) ? 1.0 / den : 0.0; // beta = 2 / v^H v (after v in slot[0..N-1])
+            slot[k] = make_double2(ph.x * (ax0 + nrm), ph.y * (ax0 + nrm)); // v_k = x0 - alpha
+#pragma unroll
+            for (int r = k + 1; r < N; ++r) slot[r] = a[r];
+            singular = singular || !(nrm > thr);
+        }
+        __syncwarp();
+        const double beta = scr[2 * N];
+        double2 sdot = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int r = k; r < N; ++r) {
+            const double2 v = slot[r];
+            sdot.x = fma(v.x, a[r].x, fma(v.y, a[r].y, sdot.x));
+            sdot.y = fma(v.x, a[r].y, fma(-v.y, a[r].x, sdot.y));
+        }
+        const double2 t = make_double2(beta * sdot.x, beta * sdot.y);
+        const bool upd = c > k;
+#pragma unroll
+        for (int r = k; r < N; ++r) {
+            const double2 v = slot[r];
+            const double2 nv = make_double2(a[r].x - (t.x * v.x - t.y * v.y), a[r].y - (t.x * v.y + t.y * v.x));
+            a[r] = upd ? nv : a[r];
+        }
+        if (c == k) {
+            a[k] = alpha;
+#pragma unroll
+            for (int r = k + 1; r < N; ++r) a[r] = make_double2(0.0, 0.0);
+        }
+        __syncwarp();
+    }
+    // R and Q^H [G_tau | h] back into the slot ([row][col]), then rows on lanes c < N
+    if (live) {
+#pragma unroll
+        for (int r = 0; r < N; ++r) slot[r * RW + c] = a[r];
+    }
+    __syncwarp();
+    const int i = (c < N) ? c : 0;
+    double2 b1 = slot[i * RW + N], b2 = slot[i * RW + N + 1];
+    b1 = make_double2(-b1.x, -b1.y);
+    b2 = make_double2(-b2.x, -b2.y);
+    const double2 rii = slot[i * RW + i];
+    const double rd = 1.0 / fma(rii.x, rii.x, rii.y * rii.y);
+    const double2 rinv = make_double2(rii.x * rd, -rii.y * rd);
+    double2 d1 = make_double2(0.0, 0.0), d2 = d1;
+#pragma unroll
+    for (int j = N - 1; j >= 0; --j) {
+        if (c == j) {
+            d1 = cmul(b1, rinv);
+            d2 = cmul(b2, rinv);
+            if (live) {
+                sm.inv[j][qc] = d1;
+                sm.out2[j][qc] = d2;
+            }
+        }
+        __syncwarp();
+        if (c < j) {
+            const double2 e1 = sm.inv[j][qc], e2 = sm.out2[j][qc], rij = slot[c * RW + j];
+            b1 = cfms(b1, rij, e1);
+            b2 = cfms(b2, rij, e2);
+        }
+    }
+    __syncwarp();
+    col = i;
+    dE = d1;
+    dN = d2;
+}
+
 template <int N, int MODE>
 __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S, const Args A)
 {
@@ -809,31 +929,43 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
             }
         }
         __syncthreads();
-        for (int g = warp; g < G::NGRP; g += G::NWARP) {
-            int col, qq;
-            double2 dE, dN;
-            bool sing, act;
-            lsolve<N>(sm, lane, warp, g, col, dE, dN, sing, act, qq);
-            if (act) {
-                if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
-                const double2 xv = sm.xs[col][qq];
-                if (MODE == MODE_DIRS) {
-                    // dx/dt = x (.) delta_E / t, dN_x = x (.) delta_N (Jx = G diag(1/x), Jt = G_tau/t)
-                    const double2 de = cmul(xv, dE), dn = cmul(xv, dN);
-                    const double ti = sm.tinv[qq];
-                    sm.inv[col][qq] = make_double2(de.x * ti, de.y * ti);
-                    sm.out2[col][qq] = dn;
-                } else if (it == 0) {
-                    // Euler: dx/dtau = x (.) delta_E  ->  x~ = x + h x delta_E
-                    const double h = (base + qq < A.P) ? A.dtau[base + qq] : 0.0;
-                    const double2 d = cmul(xv, dE);
-                    sm.xs[col][qq] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
-                } else {
-                    // Newton: x~ = x~ + x~ (.) delta_N
-                    const double2 d = cmul(xv, dN);
-                    sm.xs[col][qq] = make_double2(xv.x + d.x, xv.y + d.y);
-                    sm.dn2[col][qq] = fma(d.x, d.x, d.y * d.y);
-                }
+        auto apply = [&](int col, int qq, double2 dE, double2 dN, bool sing) {
+            if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
+            const double2 xv = sm.xs[col][qq];
+            if (MODE == MODE_DIRS) {
+                // dx/dt = x (.) delta_E / t, dN_x = x (.) delta_N (Jx = G diag(1/x), Jt = G_tau/t)
+                const double2 de = cmul(xv, dE), dn = cmul(xv, dN);
+                const double ti = sm.tinv[qq];
+                sm.inv[col][qq] = make_double2(de.x * ti, de.y * ti);
+                sm.out2[col][qq] = dn;
+            } else if (it == 0) {
+                // Euler: dx/dtau = x (.) delta_E  ->  x~ = x + h x delta_E
+                const double h = (base + qq < A.P) ? A.dtau[base + qq] : 0.0;
+                const double2 d = cmul(xv, dE);
+                sm.xs[col][qq] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
+            } else {
+                // Newton: x~ = x~ + x~ (.) delta_N
+                const double2 d = cmul(xv, dN);
+                sm.xs[col][qq] = make_double2(xv.x + d.x, xv.y + d.y);
+                sm.dn2[col][qq] = fma(d.x, d.x, d.y * d.y);
+            }
+        };
+        if (A.solver == SOLVER_QR) {
+            constexpr int NGQ = (PTS + 32 / (N + 2) - 1) / (32 / (N + 2));
+            for (int g = warp; g < NGQ; g += G::NWARP) {
+                int col, qq;
+                double2 dE, dN;
+                bool sing, act;
+                qsolve<N>(sm, lane, g, col, dE, dN, sing, act, qq);
+                if (act) apply(col, qq, dE, dN, sing);
+            }
+        } else {
+            for (int g = warp; g < G::NGRP; g += G::NWARP) {
+                int col, qq;
+                double2 dE, dN;
+                bool sing, act;
+                lsolve<N>(sm, lane, warp, g, col, dE, dN, sing, act, qq);
+                if (act) apply(col, qq, dE, dN, sing);
             }
         }
         __syncthreads();
@@ -1030,14 +1162,28 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             if (q < PTS) store_row<N>(sm, k, q, row);
         }
         __syncthreads();
-        for (int g = warp; g < G::NGRP; g += G::NWARP) {
-            int col, qq;
-            double2 dE, dN;
-            bool sing, act;
-            lsolve<N>(sm, lane, warp, g, col, dE, dN, sing, act, qq);
-            if (act) {
-                if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
-                T.dd[col][qq] = (T.phase[qq] == PH_PREDICT) ? dE : dN;
+        if (A.solver == SOLVER_QR) {
+            constexpr int NGQ = (PTS + 32 / (N + 2) - 1) / (32 / (N + 2));
+            for (int g = warp; g < NGQ; g += G::NWARP) {
+                int col, qq;
+                double2 dE, dN;
+                bool sing, act;
+                qsolve<N>(sm, lane, g, col, dE, dN, sing, act, qq);
+                if (act) {
+                    if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
+                    T.dd[col][qq] = (T.phase[qq] == PH_PREDICT) ? dE : dN;
+                }
+            }
+        } else {
+            for (int g = warp; g < G::NGRP; g += G::NWARP) {
+                int col, qq;
+                double2 dE, dN;
+                bool sing, act;
+                lsolve<N>(sm, lane, warp, g, col, dE, dN, sing, act, qq);
+                if (act) {
+                    if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
+                    T.dd[col][qq] = (T.phase[qq] == PH_PREDICT) ? dE : dN;
+                }
             }
         }
         __syncthreads();
