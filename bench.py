@@ -158,6 +158,19 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def step_traffic(points):
+    """DRAM bytes per step launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
+    ncu --set full capture of the same kernel (profiles/r01_step_traffic.json), scaled from the
+    captured launch's point count to this launch's; None if the capture is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_step_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["dram_bytes"] * points / d["points"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def cpu_baseline(seconds_target=12.0):
     """The oracle timed on a bounded sample of the same workload (rank 0, N = 1 only)."""
     import oracle
@@ -252,6 +265,8 @@ def main():
     ap.add_argument("--ref-points", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--solver", default="lu", choices=["lu", "qr"], help="direction solver (pht_system_set_solver)")
+    ap.add_argument("--specialize", action="store_true", help="system-specialised kernels (pht_system_specialize)")
     ap.add_argument("--tracking", default="katsura-10,noon-10,cyclic-10",
                     help="comma list of tracked configs ('' to skip)")
     args = ap.parse_args()
@@ -270,6 +285,9 @@ def main():
 
     sysm = _system()
     g = P.System.from_workload(sysm, device=local)
+    g.set_solver(args.solver)
+    if args.specialize:
+        g.specialize()  # NVRTC compile, outside the timed region
     Pn = args.points
     # each rank its own shard of independent points (weak scaling; seeds differ per rank)
     x_h, _, tau_h = W.random_points(Pn, N_VARS, seed=1000 + rank, tau_lo=TAU_LO)
@@ -347,10 +365,11 @@ def main():
                                    "(1 Euler prediction + 1 Newton iteration, P:911-920) on a batch of points",
                        "points_per_gpu": Pn, "n": N_VARS, "terms": sysm.M, "lift_max": LIFT_MAX,
                        "dtau": DTAU, "evals_per_point_step": 2, "parallelism": f"dp{world} (independent points)",
+                       "solver": args.solver, "specialized": bool(args.specialize),
                        "l2": "inputs larger than L2 (state %.0f MB > 126 MB)" % (Pn * (16 * N_VARS + 24) / 1e6)},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_pht<10,32,MODE_STEP>",
+                         "frac": achieved / peak, "traffic": step_traffic(Pn),
+                         "kernel": "k_pht<10, MODE_STEP>",
                          "peak_basis": f"FP64 148 SM x 64 FMA/clk x 2 x {peak_mhz:.0f} MHz (DESIGN.md §5)",
                          "flops_per_point_step": 2 * fl["total"]},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pn * (16 * N_VARS + 16),
