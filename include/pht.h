@@ -41,7 +41,7 @@ typedef enum {
     PHT_OK = 0,
     PHT_EINVAL = -1,       /* bad argument (NULL, negative size, non-finite data)        */
     PHT_ESHAPE = -2,       /* n_eq != n_var, n outside [1, PHT_MAX_N], bad offsets        */
-    PHT_EDUPLICATE = -3,   /* duplicate exponent vector inside one equation        */
+    PHT_EDUPLICATE = -3,   /* duplicate (exponent vector, lifting) term in an equation */
     PHT_EEMPTY = -4,       /* an equation has no term with a nonzero coefficient   */
     PHT_ERANGE = -5,       /* |exponent| > PHT_MAX_EXP or lifting < 0                    */
     PHT_ECUDA = -6,        /* a CUDA runtime call failed (see pht_last_cuda_error)        */

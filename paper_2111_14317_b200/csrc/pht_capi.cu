@@ -108,11 +108,13 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
     M = 0;
     n_dropped = 0;
     for (int k = 0; k < n; ++k) {
-        std::set<std::vector<int32_t>> seen;
+        // a term is (a, omega): the same monomial may appear with different liftings (the
+        // coefficient-parameter homotopy (1 - t) G + t F has x^a t^0 and x^a t^1 terms)
+        std::set<std::pair<std::vector<int32_t>, double>> seen;
         int cnt = 0;
         for (int64_t i = off[k]; i < off[k + 1]; ++i) {
             std::vector<int32_t> a(exps + i * n, exps + (i + 1) * n);
-            if (!seen.insert(a).second) return PHT_EDUPLICATE;
+            if (!seen.insert({a, lifting[i]}).second) return PHT_EDUPLICATE;
             for (int j = 0; j < n; ++j)
                 if (a[j] > PHT_MAX_EXP || a[j] < -PHT_MAX_EXP) return PHT_ERANGE;
             const double cr = coeffs[2 * i], ci = coeffs[2 * i + 1], w = lifting[i];
@@ -648,7 +650,7 @@ extern "C" const char *pht_strerror(int code)
     case PHT_OK: return "ok";
     case PHT_EINVAL: return "invalid argument";
     case PHT_ESHAPE: return "shape error (square n in [1, PHT_MAX_N], monotone offsets)";
-    case PHT_EDUPLICATE: return "duplicate monomial in an equation";
+    case PHT_EDUPLICATE: return "duplicate (monomial, lifting) term in an equation";
     case PHT_EEMPTY: return "equation without a nonzero term";
     case PHT_ERANGE: return "exponent or lifting out of range";
     case PHT_ECUDA: return "CUDA error";

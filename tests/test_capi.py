@@ -83,3 +83,18 @@ def test_specialize_codegen_without_gpu():
     assert nb > 0
     with pytest.raises(P.PhtError):
         P.specialize_compile(sysm, 64)
+
+
+def test_packer_terms_are_monomial_lifting_pairs():
+    """The same monomial with two liftings (x^a t^0 and x^a t^1 of the parameter homotopy) is two
+    terms; the same (monomial, lifting) twice is PHT_EDUPLICATE.  pht_specialize_source runs the
+    packer without a device."""
+    import numpy as np
+    from paper_2111_14317_b200 import _lib
+    lib = _lib.load()
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    off = np.array([0, 2], np.int64)
+    ex = np.array([[1], [1]], np.int32)
+    c = np.ones(2, np.complex128)
+    assert lib.pht_specialize_source(1, 1, P(off), P(ex), P(c), P(np.array([0.0, 1.0])), None, 0) > 0
+    assert lib.pht_specialize_source(1, 1, P(off), P(ex), P(c), P(np.array([1.0, 1.0])), None, 0) == -3
