@@ -100,8 +100,10 @@ int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative ph
  * the row_exp2 convention with the exponent taken from the row's largest term).
  *   what   bit set of PHT_SPEC_* (0 = all): EVAL = pht_evaluate / pht_evaluate_log,
  *          STEP = pht_euler_newton / pht_pc_step, TRACK = pht_track / pht_track_cells.
- * Host-synchronous; compile time grows with the number of terms (about a second for the n = 10
- * benchmark systems).  Calling it again with a subset of the compiled kernels is a no-op.
+ * Host-synchronous; compile time grows with the number of terms (about 4 s for the n = 10
+ * benchmark systems; images are cached per process by generated source).  Calling it again with
+ * a subset of the compiled kernels is a no-op.  The tracker uses the specialised kernel only
+ * when the batch fills at least one wave of its (larger) tiles; env PHT_JIT_TRACK=1 forces it.
  * Returns PHT_OK, PHT_EJIT (NVRTC failed: log in pht_last_cuda_error), PHT_ECUDA (load failed)
  * or PHT_EINVAL.  Not thread-safe against concurrent calls on the same handle.
  */

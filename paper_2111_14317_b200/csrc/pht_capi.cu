@@ -609,7 +609,13 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
                          o.pred_log < 0 ? o.log_state : o.pred_log};
-    if (s->jit && (pht::jit_what(s->jit) & pht::JIT_TRACK)) e = pht::jit_launch_track(s->jit, S, A, st, s->sms);
+    // the specialised tracker only with at least one full wave of paths: its tiles are 2-3x larger
+    // than the generic kernel's, so few paths would run on few SMs (measured: 70 paths 4x slower)
+    // (PHT_JIT_TRACK=1 forces it: tests)
+    const char *force = getenv("PHT_JIT_TRACK");
+    if (s->jit && (pht::jit_what(s->jit) & pht::JIT_TRACK) &&
+        (p >= pht::jit_track_slots(s->jit, s->sms) || (force && force[0] == '1')))
+        e = pht::jit_launch_track(s->jit, S, A, st, s->sms);
     else switch (s->n) {
 #define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)

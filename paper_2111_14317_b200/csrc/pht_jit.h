@@ -36,6 +36,8 @@ JitKernels *jit_load(int n, unsigned what, const std::vector<char> &cubin, const
                      cudaError_t *err);
 void jit_free(JitKernels *J);
 unsigned jit_what(const JitKernels *J);
+// path slots of one full wave of the specialised tracker (SMs x resident CTAs x points per CTA)
+int64_t jit_track_slots(const JitKernels *J, int sms);
 
 cudaError_t jit_launch(const JitKernels *J, int mode, const DevSys &S, const Args &A, cudaStream_t stream);
 cudaError_t jit_launch_track(const JitKernels *J, const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms);

@@ -24,6 +24,12 @@ def P():
     return P
 
 
+@pytest.fixture(autouse=True)
+def _jit_tracker_always(monkeypatch):
+    # the specialised tracker normally needs a full wave of paths; these small runs force it
+    monkeypatch.setenv("PHT_JIT_TRACK", "1")
+
+
 def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
