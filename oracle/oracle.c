@@ -660,15 +660,20 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             }
         }
         if (st == 0) {
-            int conv = 0;
+            /* refine at t = 1 until ||dN|| <= final_tol; an endpoint whose corrections only reach
+             * newton_tol within final_iters (the evaluation's accuracy floor at ill-conditioned
+             * endpoints) is accepted at that accuracy (reading R14) */
+            int conv = 0, solved = 1;
+            double nd = INFINITY;
             for (int it = 1; it <= final_iters; ++it) {
                 int s1 = solve_point(&s, xq, 1.0, 0, dN);
                 ++evals; ++fin;
-                if (s1) break;
-                double nd = relmax(n, dN, xq);
+                if (s1) { solved = 0; break; }
+                nd = relmax(n, dN, xq);
                 for (int i = 0; i < 2 * n; ++i) xq[i] += dN[i];
                 if (nd <= final_tol) { conv = 1; break; }
             }
+            if (!conv && solved && nd <= newton_tol) conv = 1;
             double xinf = 0.0;
             for (int j = 0; j < n; ++j) xinf = fmax(xinf, cabs(load(xq + 2 * j)));
             st = (conv && xinf <= inf_norm) ? ORC_PT_OK : ORC_PT_DIVERGED;
@@ -819,15 +824,17 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
             }
         }
         if (st == 0) {
-            int conv = 0;
+            int conv = 0, solved = 1; /* final refinement: as orc_track (reading R14) */
+            double nd = INFINITY;
             for (int it = 1; it <= final_iters; ++it) {
                 int s1 = solve_point_x(&s, xq, 0.0, wr, 0, dN);
                 ++evals; ++fin;
-                if (s1) break;
-                double nd = relmax_d(n, dN);
+                if (s1) { solved = 0; break; }
+                nd = relmax_d(n, dN);
                 xupdate(n, xq, dN, 1.0);
                 if (nd <= final_tol) { conv = 1; break; }
             }
+            if (!conv && solved && nd <= newton_tol) conv = 1;
             double lmax = -INFINITY;
             for (int j = 0; j < n; ++j) lmax = fmax(lmax, xabs_log2(xq[j]));
             st = (conv && lmax <= log2(inf_norm)) ? ORC_PT_OK : ORC_PT_DIVERGED;

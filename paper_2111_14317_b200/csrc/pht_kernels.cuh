@@ -1255,7 +1255,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                     }
                     const bool finite = LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm);
                     if (sqrt(nd) <= o.final_tol) finish = finite ? 0 : 32;
-                    else if (T.fin[qq] >= o.final_iters) finish = 32;
+                    else if (T.fin[qq] >= o.final_iters) // accuracy floor: accept at newton_tol (R14)
+                        finish = (sqrt(nd) <= o.newton_tol && finite) ? 0 : 32;
                 }
             }
             if (reject) {
