@@ -172,6 +172,61 @@ class Oracle:
         return xm, xe, tau, st, stats
 
 
+    # --- projective formulation -------------------------
+    def proj_evaluate(self, y, t):
+        """H^, dH^/dy [p, n, n+1], dH^/dt of the homogenised system (Eq. (3)) at y in C^{n+1}."""
+        y = _c2(y)
+        t = np.ascontiguousarray(t, np.float64)
+        p, n = y.shape[0], self.n
+        assert y.shape[1] == n + 1
+        out = dict(H=np.zeros((p, n), np.complex128), Jy=np.zeros((p, n, n + 1), np.complex128),
+                   Jt=np.zeros((p, n), np.complex128), SH=np.zeros((p, n)), SJy=np.zeros((p, n, n + 1)),
+                   SJt=np.zeros((p, n)), status=np.zeros(p, np.uint8))
+        rc = lib().orc_proj_evaluate(*self._sys_args(), ctypes.c_int64(p), _p(y), _p(t),
+                                     *[_p(out[k]) for k in ("H", "Jy", "Jt", "SH", "SJy", "SJt", "status")])
+        assert rc == 0
+        return out
+
+    def proj_euler_newton(self, y, t):
+        """Projective Euler E = dy/dtau and Newton N directions."""
+        y = _c2(y)
+        t = np.ascontiguousarray(t, np.float64)
+        p, m = y.shape
+        E = np.zeros((p, m), np.complex128)
+        N = np.zeros((p, m), np.complex128)
+        st = np.zeros(p, np.uint8)
+        rc = lib().orc_proj_euler_newton(*self._sys_args(), ctypes.c_int64(p), _p(y), _p(t), _p(E), _p(N), _p(st))
+        assert rc == 0
+        return E, N, st
+
+    def proj_pc_step(self, y, tau, dtau, K=1):
+        y = _c2(y).copy()
+        tau = np.ascontiguousarray(tau, np.float64).copy()
+        dtau = np.ascontiguousarray(dtau, np.float64)
+        p = y.shape[0]
+        st = np.zeros(p, np.uint8)
+        dn = np.zeros(p)
+        rc = lib().orc_proj_pc_step(*self._sys_args(), ctypes.c_int64(p), _p(y), _p(tau), _p(dtau),
+                                    ctypes.c_int(K), _p(st), _p(dn))
+        assert rc == 0
+        return y, tau, st, dn
+
+    def proj_track(self, y, tau, *, dtau_init=0.05, dtau_min=1e-12, dtau_max=0.5, newton_tol=1e-10,
+                   shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
+                   max_steps=10000, final_iters=5):
+        y = _c2(y).copy()
+        tau = np.ascontiguousarray(tau, np.float64).copy()
+        p = y.shape[0]
+        opt = np.array([dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm])
+        iopt = np.array([K, grow_after, max_steps, final_iters, 0], np.int32)
+        st = np.zeros(p, np.uint8)
+        stats = np.zeros((p, 4), np.int64)
+        rc = lib().orc_proj_track(*self._sys_args(), ctypes.c_int64(p), _p(y), _p(tau), _p(opt), _p(iopt),
+                                  _p(st), _p(stats))
+        assert rc == 0
+        return y, tau, st, stats
+
+
 # --- test plumbing (not the oracle): log coordinates <-> extended-range (mantissa, exponent) ---
 def z_to_x(z):
     """z = log x  ->  (m, e) with x = m * 2**e, |m| in [1, 2)."""

@@ -31,6 +31,10 @@
  *                     step control = DESIGN.md reading R14).
  *   orc_track_x       the same tracker with extended-range state for start points far outside
  *                     double range (polyhedral start points at large |tau0|).
+ *   orc_proj_*        the projective formulation and its directions (P:237-252,
+ *                     P:277-291): evaluation of the homogenised system, the bordered
+ *                     [dH^/dy; y^*] 2-RHS solve, the step and the tracker in homogeneous
+ *                     coordinates.
  *
  * All complex numbers are interleaved (re, im) doubles.  Arithmetic is plain C
  * double in a fixed order; OpenMP only distributes independent points/paths.
@@ -115,11 +119,12 @@ static cplx cpow_int(cplx x, cplx r, int64_t a)
 /* the system: per-equation term segments of Eq. (1)       */
 /* ------------------------------------------------------------------ */
 typedef struct {
-    int n;                 /* equations == variables                     */
+    int n;                 /* equations                                  */
     const int64_t *off;    /* [n+1] terms of eq k are [off[k], off[k+1]) */
-    const int32_t *a;      /* [M][n] integer exponents a                 */
+    const int32_t *a;      /* [M][nv] integer exponents a                */
     const double *c;       /* [M][2] coefficients c_{k,a}                */
     const int64_t *w;      /* [M] integer liftings omega_k(a) >= 0       */
+    int nv;                /* variables: n (affine) or n + 1 (projective) */
 } orc_sys;
 
 /*
@@ -134,35 +139,35 @@ static int eval_point(const orc_sys *s, const double *xp, double t,
                       double *H, double *Jx, double *Jt,
                       double *SH, double *SJx, double *SJt)
 {
-    const int n = s->n;
-    cplx x[64], r[64];
+    const int n = s->n, nv = s->nv;
+    cplx x[65], r[65];
     int st = ORC_PT_OK;
-    for (int j = 0; j < n; ++j) {
+    for (int j = 0; j < nv; ++j) {
         x[j] = load(xp + 2 * j);
         if (creal(x[j]) == 0.0 && cimag(x[j]) == 0.0) st |= ORC_PT_ZERO_COORD;
         if (!isfinite(creal(x[j])) || !isfinite(cimag(x[j]))) st |= ORC_PT_NONFINITE;
         r[j] = cdiv(mk(1.0, 0.0), x[j]);
     }
     for (int k = 0; k < n; ++k) {
-        cplx h = 0, ht = 0, hx[64];
-        double sh = 0, sht = 0, shx[64];
-        for (int j = 0; j < n; ++j) { hx[j] = 0; shx[j] = 0; }
+        cplx h = 0, ht = 0, hx[65];
+        double sh = 0, sht = 0, shx[65];
+        for (int j = 0; j < nv; ++j) { hx[j] = 0; shx[j] = 0; }
         for (int64_t i = s->off[k]; i < s->off[k + 1]; ++i) {
-            const int32_t *a = s->a + i * n;
+            const int32_t *a = s->a + i * nv;
             const cplx c = load(s->c + 2 * i);
             const int64_t w = s->w[i];
             /* the term itself: c * prod_j x_j^{a_j} * t^w */
             cplx T = c;
-            for (int j = 0; j < n; ++j)
+            for (int j = 0; j < nv; ++j)
                 if (a[j] != 0) T = cmul(T, cpow_int(x[j], r[j], a[j]));
             T = cmul(T, mk(rpow_nat(t, w), 0.0));
             h += T;
             sh += cabs(T);
             /* d/dx_j: c * a_j * prod_l x_l^{a_l - [l==j]} * t^w, from scratch */
-            for (int j = 0; j < n; ++j) {
+            for (int j = 0; j < nv; ++j) {
                 if (a[j] == 0) continue;
                 cplx D = cmul(c, mk((double)a[j], 0.0));
-                for (int l = 0; l < n; ++l) {
+                for (int l = 0; l < nv; ++l) {
                     int64_t e = a[l] - (l == j ? 1 : 0);
                     if (e != 0) D = cmul(D, cpow_int(x[l], r[l], e));
                 }
@@ -173,7 +178,7 @@ static int eval_point(const orc_sys *s, const double *xp, double t,
             /* d/dt: c * w * x^a * t^{w-1} */
             if (w >= 1) {
                 cplx D = cmul(c, mk((double)w, 0.0));
-                for (int j = 0; j < n; ++j)
+                for (int j = 0; j < nv; ++j)
                     if (a[j] != 0) D = cmul(D, cpow_int(x[j], r[j], a[j]));
                 D = cmul(D, mk(rpow_nat(t, w - 1), 0.0));
                 ht += D;
@@ -184,9 +189,9 @@ static int eval_point(const orc_sys *s, const double *xp, double t,
         if (Jt) store(Jt + 2 * k, ht);
         if (SH) SH[k] = sh;
         if (SJt) SJt[k] = sht;
-        for (int j = 0; j < n; ++j) {
-            if (Jx) store(Jx + 2 * (k * n + j), hx[j]);
-            if (SJx) SJx[k * n + j] = shx[j];
+        for (int j = 0; j < nv; ++j) {
+            if (Jx) store(Jx + 2 * (k * nv + j), hx[j]);
+            if (SJx) SJx[k * nv + j] = shx[j];
         }
     }
     return st;
@@ -198,7 +203,7 @@ int orc_evaluate(int n, const int64_t *off, const int32_t *a, const double *c, c
                  uint8_t *status)
 {
     if (n < 1 || n > 64) return -1;
-    orc_sys s = {n, off, a, c, w};
+    orc_sys s = {n, off, a, c, w, n};
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t q = 0; q < p; ++q) {
         int st = eval_point(&s, x + 2 * n * q, t[q],
@@ -340,7 +345,7 @@ int orc_evaluate_x(int n, const int64_t *off, const int32_t *a, const double *c,
                    double *Jtm, int64_t *Jte, double *LSH, double *LSJx, double *LSJt)
 {
     if (n < 1 || n > 64) return -1;
-    orc_sys s = {n, off, a, c, w};
+    orc_sys s = {n, off, a, c, w, n};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t q = 0; q < p; ++q) {
         xc x[64], H[64], Jx[64 * 64], Jt[64], SH[64], SJx[64 * 64], SJt[64];
@@ -527,7 +532,7 @@ int orc_euler_newton(int n, const int64_t *off, const int32_t *a, const double *
                      uint8_t *status)
 {
     if (n < 1 || n > 64) return -1;
-    orc_sys s = {n, off, a, c, w};
+    orc_sys s = {n, off, a, c, w, n};
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t q = 0; q < p; ++q)
         status[q] = (uint8_t)solve_point(&s, x + 2 * n * q, t[q], dE + 2 * n * q, dN + 2 * n * q);
@@ -552,7 +557,7 @@ int orc_pc_step(int n, const int64_t *off, const int32_t *a, const double *c, co
                 double *dn_norm)
 {
     if (n < 1 || n > 64) return -1;
-    orc_sys s = {n, off, a, c, w};
+    orc_sys s = {n, off, a, c, w, n};
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t q = 0; q < p; ++q) {
         double *xq = x + 2 * n * q, dE[128] = {0}, dN[128] = {0}, xt[128];
@@ -602,7 +607,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
               uint8_t *status, int64_t *stats)
 {
     if (n < 1 || n > 64) return -1;
-    orc_sys s = {n, off, a, c, w};
+    orc_sys s = {n, off, a, c, w, n};
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
@@ -767,7 +772,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                 uint8_t *status, int64_t *stats, const double *cellw, const int32_t *path_cell)
 {
     if (n < 1 || n > 64) return -1;
-    orc_sys s = {n, off, a, c, w};
+    orc_sys s = {n, off, a, c, w, n};
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
@@ -854,6 +859,246 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
 #include <omp.h>
 #endif
 /* Thread count used by the parallel-for loops (timing only; results do not depend on it). */
+/* ------------------------------------------------------------------ */
+/* projective formulation (Eq. (3)) and its directions      */
+/* (P:237-252): y in C^{n+1}, homogenising coordinate LAST  */
+/* (SURVEY A8), a^ = (a, deg(f_k) - 1^T a) with deg(f_k) = max 1^T a.   */
+/* ------------------------------------------------------------------ */
+
+/* a^ for every term: int32 [M][n+1] (caller frees). */
+static int32_t *homogenize(int n, const int64_t *off, const int32_t *a)
+{
+    const int64_t M = off[n];
+    int32_t *ah = (int32_t *)malloc(sizeof(int32_t) * (size_t)(M > 0 ? M : 1) * (n + 1));
+    if (!ah) return 0;
+    for (int k = 0; k < n; ++k) {
+        int64_t deg = INT64_MIN;
+        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
+            int64_t d = 0;
+            for (int j = 0; j < n; ++j) d += a[i * n + j];
+            if (d > deg) deg = d;
+        }
+        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
+            int64_t d = 0;
+            for (int j = 0; j < n; ++j) {
+                ah[i * (n + 1) + j] = a[i * n + j];
+                d += a[i * n + j];
+            }
+            ah[i * (n + 1) + n] = (int32_t)(deg - d);
+        }
+    }
+    return ah;
+}
+
+/* H^, dH^/dy (n x (n+1)), dH^/dt at homogeneous points y (Eq. (3)). */
+int orc_proj_evaluate(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
+                      int64_t p, const double *y, const double *t, double *H, double *Jy, double *Jt,
+                      double *SH, double *SJy, double *SJt, uint8_t *status)
+{
+    if (n < 1 || n > 63) return -1;
+    int32_t *ah = homogenize(n, off, a);
+    if (!ah) return -2;
+    orc_sys s = {n, off, ah, c, w, n + 1};
+    const int m = n + 1;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < p; ++q) {
+        int st = eval_point(&s, y + 2 * m * q, t[q], H ? H + 2 * n * q : 0, Jy ? Jy + 2 * n * m * q : 0,
+                            Jt ? Jt + 2 * n * q : 0, SH ? SH + n * q : 0, SJy ? SJy + n * m * q : 0,
+                            SJt ? SJt + n * q : 0);
+        if (status) status[q] = (uint8_t)st;
+    }
+    free(ah);
+    return 0;
+}
+
+/*
+ * Projective Euler and Newton directions: one LU solve with two
+ * right-hand sides of the bordered (n+1) x (n+1) system
+ *     [ dH^/dy ] [E N] = - [ dH^/dtau  H^ ]        dH^/dtau = t dH^/dt  (tau = log t)
+ *     [  y^*   ]           [    0       0 ]
+ * y^* = row of conjugated coordinates.  E = dy/dtau, N = the projective Newton direction.
+ */
+static int proj_solve_point(const orc_sys *s, const double *yp, double t, double *E, double *N)
+{
+    const int n = s->n, m = n + 1;
+    double H[128], Jy[64 * 65 * 2], Jt[128], A[65 * 65 * 2], B[65 * 2 * 2], X[65 * 2 * 2];
+    int st = eval_point(s, yp, t, H, Jy, Jt, 0, 0, 0);
+    if (st) return st;
+    for (int k = 0; k < n; ++k) {
+        for (int j = 0; j < m; ++j) store(A + 2 * (k * m + j), load(Jy + 2 * (k * m + j)));
+        store(B + 2 * (k * 2 + 0), mk(-t * Jt[2 * k], -t * Jt[2 * k + 1]));
+        store(B + 2 * (k * 2 + 1), mk(-H[2 * k], -H[2 * k + 1]));
+    }
+    for (int j = 0; j < m; ++j) store(A + 2 * (n * m + j), conj(load(yp + 2 * j)));
+    store(B + 2 * (n * 2 + 0), mk(0.0, 0.0));
+    store(B + 2 * (n * 2 + 1), mk(0.0, 0.0));
+    st = orc_lu_solve(m, 2, A, B, X);
+    if (st) return st;
+    for (int j = 0; j < m; ++j) {
+        if (E) store(E + 2 * j, load(X + 2 * (j * 2)));
+        if (N) store(N + 2 * j, load(X + 2 * (j * 2 + 1)));
+    }
+    for (int k = 0; k < 2 * m; ++k)
+        if ((E && !isfinite(E[k])) || (N && !isfinite(N[k]))) return ORC_PT_NONFINITE;
+    return 0;
+}
+
+int orc_proj_euler_newton(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
+                          int64_t p, const double *y, const double *t, double *E, double *N, uint8_t *status)
+{
+    if (n < 1 || n > 63) return -1;
+    int32_t *ah = homogenize(n, off, a);
+    if (!ah) return -2;
+    orc_sys s = {n, off, ah, c, w, n + 1};
+    const int m = n + 1;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < p; ++q)
+        status[q] = (uint8_t)proj_solve_point(&s, y + 2 * m * q, t[q], E + 2 * m * q, N + 2 * m * q);
+    free(ah);
+    return 0;
+}
+
+/* y <- y / ||y|| (points of P^n are kept on the unit sphere, reading R29) */
+static void proj_normalize(int m, double *y)
+{
+    double s2 = 0.0;
+    for (int i = 0; i < 2 * m; ++i) s2 += y[i] * y[i];
+    const double f = 1.0 / sqrt(s2);
+    for (int i = 0; i < 2 * m; ++i) y[i] *= f;
+}
+
+/*
+ * The Euler-Newton step in homogeneous coordinates: y~ = y + h E; tau~ = tau + h;
+ * K times y~ += N(y~, tau~); y is renormalised to ||y|| = 1 after every update (reading R29).
+ * dn_norm = ||N|| of the last Newton iteration (relative to ||y|| = 1).
+ */
+int orc_proj_pc_step(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
+                     int64_t p, double *y, double *tau, const double *dtau, int K, uint8_t *status,
+                     double *dn_norm)
+{
+    if (n < 1 || n > 63) return -1;
+    int32_t *ah = homogenize(n, off, a);
+    if (!ah) return -2;
+    orc_sys s = {n, off, ah, c, w, n + 1};
+    const int m = n + 1;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < p; ++q) {
+        double *yq = y + 2 * m * q, E[130] = {0}, N[130] = {0}, yt[130];
+        const double h = dtau[q];
+        int st = proj_solve_point(&s, yq, exp(tau[q]), E, 0);
+        for (int i = 0; i < 2 * m; ++i) yt[i] = yq[i] + h * E[i];
+        proj_normalize(m, yt);
+        const double tt = tau[q] + h;
+        double nrm = 0.0;
+        for (int it = 0; it < K; ++it) {
+            st |= proj_solve_point(&s, yt, exp(tt), 0, N);
+            for (int i = 0; i < 2 * m; ++i) yt[i] += N[i];
+            nrm = vnorm(m, N);
+            proj_normalize(m, yt);
+        }
+        memcpy(yq, yt, sizeof(double) * 2 * m);
+        tau[q] = tt;
+        status[q] = (uint8_t)st;
+        if (dn_norm) dn_norm[q] = nrm;
+    }
+    free(ah);
+    return 0;
+}
+
+/*
+ * Adaptive tracking in homogeneous coordinates: orc_track's control flow (reading R14) with
+ * the projective directions, y renormalised after every update, norm-relative corrector tests
+ * (||dy|| / ||y|| <= newton_tol; componentwise tests are meaningless for coordinates going to
+ * 0 at infinity), and the endpoint classified finite iff |y_n| >= ||y|| / inf_norm (the affine
+ * point y_{0..n-1} / y_n has norm <= inf_norm), else DIVERGED: a solution at infinity.
+ * Affine Euler predictor only (pred_log is ignored).
+ */
+int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
+                   int64_t p, double *y, double *tau, const double *opt, const int32_t *iopt,
+                   uint8_t *status, int64_t *stats)
+{
+    if (n < 1 || n > 63) return -1;
+    int32_t *ah = homogenize(n, off, a);
+    if (!ah) return -2;
+    orc_sys s = {n, off, ah, c, w, n + 1};
+    const int m = n + 1;
+    const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
+    const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
+    const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < p; ++q) {
+        double *yq = y + 2 * m * q, E[130], N[130], yt[130];
+        double tq = tau[q], dt = dtau_init;
+        int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
+        int succ = 0, st = 0;
+        if (!isfinite(tq)) {
+            status[q] = ORC_PT_NONFINITE;
+            for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
+            continue;
+        }
+        proj_normalize(m, yq);
+        while (tq < 0.0) {
+            if (steps == max_steps) { st = ORC_PT_MAX_STEPS; break; }
+            double h = fmin(dt, -tq);
+            int s1 = proj_solve_point(&s, yq, exp(tq), E, 0);
+            ++evals;
+            int ok = 0;
+            double tt = tq + h;
+            if (!s1) {
+                double prev = INFINITY;
+                for (int i = 0; i < 2 * m; ++i) yt[i] = yq[i] + h * E[i];
+                proj_normalize(m, yt);
+                for (int it = 1; it <= K; ++it) {
+                    s1 = proj_solve_point(&s, yt, exp(tt), 0, N);
+                    ++evals;
+                    if (s1) break;
+                    double nd = vnorm(m, N); /* ||y~|| = 1 */
+                    for (int i = 0; i < 2 * m; ++i) yt[i] += N[i];
+                    proj_normalize(m, yt);
+                    if (nd <= newton_tol) { ok = 1; break; }
+                    if (it >= 2 && nd > 0.5 * prev) break;
+                    prev = nd;
+                }
+            }
+            if (ok) {
+                memcpy(yq, yt, sizeof(double) * 2 * m);
+                tq = tt;
+                ++steps;
+                if (++succ == grow_after) { dt = fmin(grow * dt, dtau_max); succ = 0; }
+            } else {
+                ++rejects;
+                dt *= shrink;
+                succ = 0;
+                if (dt < dtau_min) { st = (s1 & ORC_PT_SINGULAR) ? ORC_PT_SINGULAR : ORC_PT_STEP_UNDERFLOW; break; }
+            }
+        }
+        if (st == 0) {
+            int conv = 0, solved = 1;
+            double nd = INFINITY;
+            for (int it = 1; it <= final_iters; ++it) {
+                int s1 = proj_solve_point(&s, yq, 1.0, 0, N);
+                ++evals; ++fin;
+                if (s1) { solved = 0; break; }
+                nd = vnorm(m, N);
+                for (int i = 0; i < 2 * m; ++i) yq[i] += N[i];
+                proj_normalize(m, yq);
+                if (nd <= final_tol) { conv = 1; break; }
+            }
+            if (!conv && solved && nd <= newton_tol) conv = 1;
+            const double yn = hypot(yq[2 * n], yq[2 * n + 1]);
+            st = (conv && yn * inf_norm >= 1.0) ? ORC_PT_OK : ORC_PT_DIVERGED;
+        }
+        tau[q] = tq;
+        status[q] = (uint8_t)st;
+        stats[4 * q + 0] = steps;
+        stats[4 * q + 1] = rejects;
+        stats[4 * q + 2] = evals;
+        stats[4 * q + 3] = fin;
+    }
+    free(ah);
+    return 0;
+}
+
 int orc_set_threads(int nt)
 {
 #ifdef _OPENMP
