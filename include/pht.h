@@ -80,6 +80,27 @@ int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *eq_offsets,
                       const int32_t *exponents, const double *coeffs, const double *lifting,
                       int32_t device, pht_system **out);
 
+/*
+ * Projective system: the same inputs as pht_system_create (the AFFINE system),
+ * lifted into P^n as in Eq. (3): y in C^{n+1} with the homogenising coordinate LAST,
+ * exponents a^ = (a, deg(f_k) - 1^T a), deg(f_k) = max 1^T a over S_k.  Every entry point then
+ * works in homogeneous coordinates with n_var = n_eq + 1 columns (pht_system_info reports it):
+ *   pht_evaluate        H (n+1 entries, the last 0), Jx = the bordered (n+1) x (n+1) matrix
+ *                       [dH^/dy ; y^*] (last row: conjugated coordinates), Jt (last 0);
+ *   pht_euler_newton    the projective Euler / Newton directions of P:237-252 / P:277-291
+ *                       (bordered 2-RHS solve: dH^/dy E = -dH^/dtau ... with y^* E = 0);
+ *   pht_pc_step         the Euler-Newton step in y with y renormalised to ||y|| = 1 after every
+ *                       update (reading R29);
+ *   pht_track           y state only (log_state / pht_track_cells: PHT_EUNSUPPORTED); norm-
+ *                       relative corrector tests; an endpoint is finite iff |y_n| >= 1/inf_norm
+ *                       (||y|| = 1), else PHT_PT_DIVERGED: a solution at infinity, which the
+ *                       projective tracker reaches instead of losing the path.
+ * Requires n_eq + 1 <= PHT_MAX_N.  No FP64 tensor-core evaluation path.
+ */
+int pht_system_create_projective(int32_t n_eq, int32_t n_var, const int64_t *eq_offsets,
+                                 const int32_t *exponents, const double *coeffs, const double *lifting,
+                                 int32_t device, pht_system **out);
+
 /* Free the device tables.  NULL is a no-op.  No call may be in flight on the handle. */
 void pht_system_destroy(pht_system *sys);
 
@@ -87,6 +108,7 @@ void pht_system_destroy(pht_system *sys);
 #define PHT_SYS_DENSE 1 /* evaluation uses the FP64 tensor-core (DMMA) path: n >= 10 and no zero
                            coefficient dropped (env PHT_DENSE=0/1 overrides) */
 #define PHT_SYS_SPECIALIZED 2 /* system-specialised kernels loaded (pht_system_specialize) */
+#define PHT_SYS_PROJECTIVE 4  /* created by pht_system_create_projective */
 int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative pht_status */
 
 /*

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PHT_LIB") or os.path.join(_HERE, "lib", "libpht.so")
 PHT_MAX_N = 24
 PT_OK, PT_ZERO_COORD, PT_NONFINITE, PT_SINGULAR = 0, 1, 2, 4
 PT_STEP_UNDERFLOW, PT_MAX_STEPS, PT_DIVERGED = 8, 16, 32
-SYS_DENSE, SYS_SPECIALIZED = 1, 2
+SYS_DENSE, SYS_SPECIALIZED, SYS_PROJECTIVE = 1, 2, 4
 SPEC_EVAL, SPEC_STEP, SPEC_TRACK, SPEC_ALL = 1, 2, 4, 7
 SOLVER_LU, SOLVER_QR = 0, 1
 
@@ -27,6 +27,7 @@ _i64 = ctypes.c_int64
 # name -> (restype, argtypes); mirrors include/pht.h exactly
 SIGNATURES = {
     "pht_system_create": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(_vp)]),
+    "pht_system_create_projective": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(_vp)]),
     "pht_system_destroy": (None, [_vp]),
     "pht_system_info": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "pht_system_flags": (ctypes.c_int, [_vp]),

@@ -26,7 +26,7 @@ def _stream(device):
 class System:
     """A loaded homotopy (pht_system_create).  Arguments as in include/pht.h."""
 
-    def __init__(self, offsets, exponents, coeffs, lifting, device: int = 0):
+    def __init__(self, offsets, exponents, coeffs, lifting, device: int = 0, projective: bool = False):
         lib = _lib.load()
         self._lib = lib
         off = np.ascontiguousarray(offsets, np.int64)
@@ -35,7 +35,8 @@ class System:
         w = np.ascontiguousarray(lifting, np.float64)
         n = int(exps.shape[1])
         h = ctypes.c_void_p()
-        rc = lib.pht_system_create(len(off) - 1, n, off.ctypes.data_as(ctypes.c_void_p),
+        create = lib.pht_system_create_projective if projective else lib.pht_system_create
+        rc = create(len(off) - 1, n, off.ctypes.data_as(ctypes.c_void_p),
                                    exps.ctypes.data_as(ctypes.c_void_p), c.ctypes.data_as(ctypes.c_void_p),
                                    w.ctypes.data_as(ctypes.c_void_p), int(device), ctypes.byref(h))
         check(rc, "pht_system_create")
@@ -63,8 +64,13 @@ class System:
         return bool(self._lib.pht_system_flags(self._h) & _lib.SYS_SPECIALIZED)
 
     @classmethod
-    def from_workload(cls, system, device: int = 0):
-        return cls(system.offsets, system.exps, system.coeffs, system.lifting, device)
+    def from_workload(cls, system, device: int = 0, projective: bool = False):
+        return cls(system.offsets, system.exps, system.coeffs, system.lifting, device, projective)
+
+    @property
+    def projective(self) -> bool:
+        """Projective system (pht_system_create_projective): points are y in C^{n_eq + 1}."""
+        return bool(self._lib.pht_system_flags(self._h) & _lib.SYS_PROJECTIVE)
 
     def close(self):
         if getattr(self, "_h", None):

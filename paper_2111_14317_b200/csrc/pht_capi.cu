@@ -6,6 +6,7 @@
 #include "pht_kernels.cuh"
 
 #include <algorithm>
+#include <cstdint>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -39,6 +40,7 @@ struct pht_system {
     int sms = 148;
     int dropped = 0; // terms with c = 0 removed by the packer
     int solver = 0;  // PHT_SOLVER_LU / PHT_SOLVER_QR (pht_system_set_solver)
+    int proj = 0;    // projective system: n = n_eq + 1 homogeneous coordinates
     double2 *d_rec = nullptr;
     int *d_off = nullptr;
     double *d_exptab = nullptr;
@@ -90,7 +92,7 @@ struct DevGuard {
 //   [a_0 .. a_{n-1}, omega, log|c|, arg c, pad]   (DESIGN.md §2 "HBM/L1 layout")
 static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps, const double *coeffs,
                        const double *lifting, std::vector<double> &rec, std::vector<int> &doff, int &max_terms,
-                       int64_t &M, int &n_dropped)
+                       int64_t &M, int &n_dropped, bool homog = false)
 {
     if (!off || !exps || !coeffs || !lifting) return PHT_EINVAL;
     if (n_eq != n_var || n_eq < 1 || n_eq > PHT_MAX_N) return PHT_ESHAPE;
@@ -100,7 +102,11 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
         if (off[k + 1] < off[k]) return PHT_ESHAPE;
     const int64_t M_in = off[n];
     if (M_in >= (int64_t)1 << 30) return PHT_ESHAPE;
-    const int RS = pht::rec_stride(n);
+    // projective: records over y in C^{n+1}, a^ = (a, deg(f_k) - 1^T a), homogenising
+    // coordinate last, deg(f_k) = max 1^T a over the equation's terms
+    const int NV = homog ? n + 1 : n;
+    if (NV > PHT_MAX_N) return PHT_ESHAPE;
+    const int RS = pht::rec_stride(NV);
     rec.clear();
     doff.assign(n + 1, 0);
     max_terms = 0;
@@ -108,6 +114,12 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
     M = 0;
     n_dropped = 0;
     for (int k = 0; k < n; ++k) {
+        int64_t deg = INT64_MIN;
+        for (int64_t i = off[k]; i < off[k + 1]; ++i) {
+            int64_t d = 0;
+            for (int j = 0; j < n; ++j) d += exps[i * n + j];
+            deg = std::max(deg, d);
+        }
         // a term is (a, omega): the same monomial may appear with different liftings (the
         // coefficient-parameter homotopy (1 - t) G + t F has x^a t^0 and x^a t^1 terms)
         std::set<std::pair<std::vector<int32_t>, double>> seen;
@@ -121,11 +133,19 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
             if (!std::isfinite(cr) || !std::isfinite(ci) || !std::isfinite(w)) return PHT_EINVAL;
             if (w < 0) return PHT_ERANGE;
             if (cr == 0.0 && ci == 0.0) { ++n_dropped; continue; }
-            for (int j = 0; j < n; ++j) rec.push_back((double)a[j]);
+            int64_t d = 0;
+            for (int j = 0; j < n; ++j) {
+                rec.push_back((double)a[j]);
+                d += a[j];
+            }
+            if (homog) {
+                if (deg - d > PHT_MAX_EXP) return PHT_ERANGE;
+                rec.push_back((double)(deg - d));
+            }
             rec.push_back(w);
             rec.push_back(std::log(std::hypot(cr, ci)));
             rec.push_back(std::atan2(ci, cr));
-            for (int u = n + 3; u < RS; ++u) rec.push_back(0.0);
+            for (int u = NV + 3; u < RS; ++u) rec.push_back(0.0);
             ++cnt;
             ++M;
         }
@@ -136,18 +156,17 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
     return PHT_OK;
 }
 
-extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
-                                 const double *coeffs, const double *lifting, int32_t device,
-                                 pht_system **out)
+static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps, const double *coeffs,
+                       const double *lifting, int32_t device, pht_system **out, bool proj)
 {
     if (!out) return PHT_EINVAL;
     std::vector<double> rec;
     std::vector<int> doff;
     int max_terms = 0, n_dropped = 0;
     int64_t M = 0;
-    const int prc = pack_system(n_eq, n_var, off, exps, coeffs, lifting, rec, doff, max_terms, M, n_dropped);
+    const int prc = pack_system(n_eq, n_var, off, exps, coeffs, lifting, rec, doff, max_terms, M, n_dropped, proj);
     if (prc != PHT_OK) return prc;
-    const int n = n_eq;
+    const int n = proj ? n_eq + 1 : n_eq; // kernel width: variables (rows = n_eq polynomials + y^*)
 
     // exp / cis tables, rounded from 80-bit long double
     std::vector<double> etab(256), ctab(512);
@@ -167,6 +186,7 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     s->max_terms = max_terms;
     s->device = device;
     s->dropped = n_dropped;
+    s->proj = proj ? 1 : 0;
     s->h_rec = rec;
     s->h_off = doff;
     cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device);
@@ -185,8 +205,8 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     // tensor-core evaluation policy: every system with n >= 10 (measured faster than the scalar
     // kernel from n = 10 on, dense or sparse: profiles/r01_dense_tuning.txt); PHT_DENSE=0/1 overrides
     {
-        int want = (n >= 10 && n_dropped == 0) ? 1 : 0;
-        if (const char *ev = getenv("PHT_DENSE")) want = (ev[0] == '1') && n_dropped == 0;
+        int want = (n >= 10 && n_dropped == 0 && !proj) ? 1 : 0;
+        if (const char *ev = getenv("PHT_DENSE")) want = (ev[0] == '1') && n_dropped == 0 && !proj;
         if (want) {
             const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;
             std::vector<int> ntoff(n + 1, 0);
@@ -248,6 +268,20 @@ extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off
     return PHT_OK;
 }
 
+extern "C" int pht_system_create(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
+                                 const double *coeffs, const double *lifting, int32_t device,
+                                 pht_system **out)
+{
+    return create_impl(n_eq, n_var, off, exps, coeffs, lifting, device, out, false);
+}
+
+extern "C" int pht_system_create_projective(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps,
+                                            const double *coeffs, const double *lifting, int32_t device,
+                                            pht_system **out)
+{
+    return create_impl(n_eq, n_var, off, exps, coeffs, lifting, device, out, true);
+}
+
 extern "C" void pht_system_destroy(pht_system *s)
 {
     if (!s) return;
@@ -286,6 +320,7 @@ extern "C" int pht_system_flags(const pht_system *s)
     if (!s) return PHT_EINVAL;
     int f = s->dense ? PHT_SYS_DENSE : 0;
     if (s->jit) f |= PHT_SYS_SPECIALIZED;
+    if (s->proj) f |= PHT_SYS_PROJECTIVE;
     return f;
 }
 
@@ -386,7 +421,7 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     if (A0.P == 0) return PHT_OK;
     DevGuard g(s->device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
-    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj};
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     pht::Args A = A0;
@@ -583,6 +618,8 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     if (opts) o = *opts;
     else pht_track_opts_default(&o);
     if (cellw) o.log_state = 1; // cell coordinates w are logarithmic
+    if (s->proj && (cellw || o.log_state)) return PHT_EUNSUPPORTED; // projective: y state only
+    if (s->proj) o.pred_log = 0;
     if (!(o.dtau_init > 0) || !(o.dtau_min > 0) || !(o.dtau_max > 0) || !(o.shrink > 0 && o.shrink < 1) ||
         !(o.grow >= 1) || o.newton_iters < 1 || o.grow_after < 1 || o.max_steps < 1 || o.final_iters < 0)
         return PHT_EINVAL;
@@ -593,7 +630,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     cudaError_t e;
     if ((e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
-    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n};
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj};
     pht::TrackArgs A{};
     A.P = p;
     A.x = (double2 *)x;

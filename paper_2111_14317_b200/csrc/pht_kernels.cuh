@@ -55,6 +55,7 @@ struct DevSys {
     const double *exptab;  // [256] 2^(j/256)
     const double2 *cistab; // [256] (cos, sin)(2 pi j / 256)
     int n;
+    int proj; // projective system: N = n_eq + 1 homogeneous coordinates, row N-1 = y^*
 };
 
 struct Args {
@@ -515,6 +516,16 @@ template <int N>
 __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int k, int q,
                                          double2 (&row)[N + 2], int &e, const double *wq = nullptr)
 {
+    if (S.proj && k == N - 1) {
+        // the bordering row y^* of the projective directions in log
+        // coordinates: y^* (y (.) delta) = sum_j |y_j|^2 delta_j; no dH/dtau, no H entry
+#pragma unroll
+        for (int j = 0; j < N; ++j) row[j] = make_double2(exp(2.0 * sm.rt[j][q].x), 0.0);
+        row[N] = make_double2(0.0, 0.0);
+        row[N + 1] = make_double2(0.0, 0.0);
+        e = 0;
+        return;
+    }
 #ifdef PHT_JIT
     jit_row<N>(S, sm, k, q, row, e, wq);
     return;
@@ -701,6 +712,18 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
     const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
     dE = make_double2(-e.x, -e.y);
     dN = make_double2(-n.x, -n.y);
+}
+
+// y <- y / ||y|| for the point q of a [variable][point] tile (projective systems, reading R29)
+template <int N, int WLP>
+__device__ __forceinline__ void proj_normalize(double2 (*v)[WLP], int q)
+{
+    double s2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s2 = fma(v[j][q].x, v[j][q].x, fma(v[j][q].y, v[j][q].y, s2));
+    const double f = (s2 > 0.0 && isfinite(s2)) ? rsqrt(s2) : 1.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j][q] = make_double2(v[j][q].x * f, v[j][q].y * f);
 }
 
 // a5, QR route (the paper's mechanism P:708-726, Alg. 3).
@@ -969,6 +992,10 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
             }
         }
         __syncthreads();
+        if (MODE == MODE_STEP && S.proj) { // points of P^n stay on ||y|| = 1 (reading R29)
+            if (tid < PTS) proj_normalize<N>(sm.xs, tid);
+            __syncthreads();
+        }
         if (MODE == MODE_STEP && it == 0 && tid < PTS)
             sm.tau[tid] += (base + tid < A.P) ? A.dtau[base + tid] : 0.0;
     }
@@ -1138,6 +1165,10 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
         }
         __syncthreads();
         if (tid < WL) {
+            if (S.proj && tid < PTS && T.refill[tid]) { // new projective path: onto ||y|| = 1
+                proj_normalize<N>(T.xa, tid);
+                for (int j = 0; j < N; ++j) sm.xs[j][tid] = T.xa[j][tid];
+            }
             T.done_path[tid] = -1;
             T.acc[tid] = 0;
             T.refill[tid] = 0;
@@ -1198,15 +1229,25 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                     T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], dl, h)
                                              : trk_update<N, LOGS>(T.xa[j][qq], dl, h);
                 } else if (ph == PH_CORRECT) {
-                    T.xt[j][qq] = trk_update<N, LOGS>(T.xt[j][qq], dl, 1.0);
-                    T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_j / x_j|^2 (reading R14)
+                    const double2 v = T.xt[j][qq];
+                    T.xt[j][qq] = trk_update<N, LOGS>(v, dl, 1.0);
+                    // |dx_j / x_j|^2 (reading R14); projective: |dy_j|^2 with ||y|| = 1 (R29)
+                    const double r2 = fma(dl.x, dl.x, dl.y * dl.y);
+                    T.nd2[j][qq] = S.proj ? r2 * fma(v.x, v.x, v.y * v.y) : r2;
                 } else { // FINAL
-                    T.xa[j][qq] = trk_update<N, LOGS>(T.xa[j][qq], dl, 1.0);
-                    T.nd2[j][qq] = fma(dl.x, dl.x, dl.y * dl.y);
+                    const double2 v = T.xa[j][qq];
+                    T.xa[j][qq] = trk_update<N, LOGS>(v, dl, 1.0);
+                    const double r2 = fma(dl.x, dl.x, dl.y * dl.y);
+                    T.nd2[j][qq] = S.proj ? r2 * fma(v.x, v.x, v.y * v.y) : r2;
                 }
             }
         }
         __syncthreads();
+        if (S.proj) { // updated points back onto ||y|| = 1 (x state only, reading R29)
+            if (tid < PTS && sm.st[tid] == 0 && T.phase[tid] != PH_IDLE)
+                proj_normalize<N>(T.phase[tid] == PH_FINAL ? T.xa : T.xt, tid);
+            __syncthreads();
+        }
         // (4) per-slot decisions (the oracle's control flow, oracle.c orc_track)
         if (tid < PTS && T.phase[tid] != PH_IDLE) {
             const int qq = tid;
@@ -1227,8 +1268,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 if (bad) reject = true;
                 else {
                     double nd = 0.0; // max_j |dx_j| / |x_j| (componentwise relative, reading R14)
-                    for (int j = 0; j < N; ++j) nd = fmax(nd, T.nd2[j][qq]);
-                    nd = sqrt(nd);
+                    for (int j = 0; j < N; ++j) nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
+                    nd = sqrt(nd);      // projective: ||dy|| (||y|| = 1, reading R29)
                     if (nd <= o.newton_tol) {
                         T.acc[qq] = 1;
                         T.tau_a[qq] = T.tau_t[qq];
@@ -1249,11 +1290,13 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 else {
                     double nd = 0.0, xinf = 0.0; // xinf: max |x_j| (or max Re z_j in log state)
                     for (int j = 0; j < N; ++j) {
-                        nd = fmax(nd, T.nd2[j][qq]);
+                        nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
                         const double2 v = T.xa[j][qq];
                         xinf = fmax(xinf, LOGS ? v.x : sqrt(fma(v.x, v.x, v.y * v.y)));
                     }
-                    const bool finite = LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm);
+                    const double2 yn = T.xa[N - 1][qq]; // projective: finite iff |y_n| >= 1 / inf_norm
+                    const bool finite = S.proj ? (sqrt(fma(yn.x, yn.x, yn.y * yn.y)) * o.inf_norm >= 1.0)
+                                               : (LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm));
                     if (sqrt(nd) <= o.final_tol) finish = finite ? 0 : 32;
                     else if (T.fin[qq] >= o.final_iters) // accuracy floor: accept at newton_tol (R14)
                         finish = (sqrt(nd) <= o.newton_tol && finite) ? 0 : 32;
