@@ -253,13 +253,14 @@ def tracking_section(world, rank, dev, which):
                          "evals": int(sts[:, 2].sum()), "evals_per_s": float(sts[:, 2].sum() / (t * 1e-3)),
                          "state": "cell coordinates (pht_track_cells), log-chart Euler predictor, default opts"}
         if name == "cyclic-10":
-            r2 = _second_stage(world, rank, dev, sysm, L, zl, st)
-            if rank == 0:
-                out["cyclic-10 native (stage 2)"] = r2
+            for proj in (False, True):
+                r2 = _second_stage(world, rank, dev, sysm, L, zl, st, proj)
+                if rank == 0:
+                    out["cyclic-10 native (stage 2%s)" % (", projective" if proj else "")] = r2
     return out
 
 
-def _second_stage(world, rank, dev, G, L, zl, st):
+def _second_stage(world, rank, dev, G, L, zl, st, proj=False):
     """Stage 2: the coefficient-parameter homotopy (1 - t) G + t F from this
     rank's finite stage-1 endpoints to the NATIVE cyclic-10 system (pht_track, log state);
     one all_reduce of the status histogram."""
@@ -269,17 +270,20 @@ def _second_stage(world, rank, dev, G, L, zl, st):
     import workloads as W
     from workloads import param as PH
     F = W.cyclic(10, lift_max=L, coeffs="native")
-    g2 = P.System.from_workload(PH.parameter_homotopy(G, F.coeffs), device=dev.index)
+    g2 = P.System.from_workload(PH.parameter_homotopy(G, F.coeffs), device=dev.index, projective=proj)
     z = zl[st == 0].contiguous()
     t2 = torch.full((z.shape[0],), PH.TAU0, dtype=torch.float64, device=dev)
-    g2.track(z[:64].clone(), t2[:64].clone(), log_state=1)   # warm-up
+    opts = {} if proj else {"log_state": 1}
+    if proj:  # onto P^n on the device (pht_homogenize), outside the timed region like the start data
+        z = g2.homogenize(z, log_input=True)
+    g2.track(z[:64].clone(), t2[:64].clone(), **opts)   # warm-up
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    s2, stats2 = g2.track(z, t2, log_state=1)
+    s2, stats2 = g2.track(z, t2, **opts)
     hist = torch.stack([(s2 == v).sum() for v in (0, 2, 4, 8, 16, 32)]).to(torch.int64)
     if world > 1:
         dist.all_reduce(hist)
@@ -297,7 +301,8 @@ def _second_stage(world, rank, dev, G, L, zl, st):
             "paths": int(n2.item()), "ms": t, "paths_per_s": int(n2.item()) / (t * 1e-3),
             "status": dict(zip(["finite", "nonfinite", "singular", "step_underflow", "max_steps", "diverged"],
                                [int(v) for v in h])),
-            "state": "log coordinates (pht_track, log_state=1), t0 = e^-37"}
+            "state": ("homogeneous coordinates on ||y|| = 1 (pht_system_create_projective, P:187-291)" if proj
+                      else "log coordinates (pht_track, log_state=1)") + ", t0 = e^-37"}
 
 
 def main():

@@ -101,6 +101,13 @@ int pht_system_create_projective(int32_t n_eq, int32_t n_var, const int64_t *eq_
                                  const int32_t *exponents, const double *coeffs, const double *lifting,
                                  int32_t device, pht_system **out);
 
+/* Affine points of a projective system's n_eq variables onto P^n: y = (x, 1) / ||(x, 1)||
+ * (homogenising coordinate last), x = e^z when log_input (z = log x, e.g. the endpoints of
+ * pht_track_cells).  x: c128[p][n_eq] device, y: c128[p][n_eq + 1] device, async on stream.
+ * PHT_EINVAL if sys is not projective. */
+int pht_homogenize(const pht_system *sys, int64_t p, const double *x, int32_t log_input, double *y,
+                   void *stream);
+
 /* Free the device tables.  NULL is a no-op.  No call may be in flight on the handle. */
 void pht_system_destroy(pht_system *sys);
 

@@ -28,6 +28,7 @@ _i64 = ctypes.c_int64
 SIGNATURES = {
     "pht_system_create": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(_vp)]),
     "pht_system_create_projective": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(_vp)]),
+    "pht_homogenize": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, _vp]),
     "pht_system_destroy": (None, [_vp]),
     "pht_system_info": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "pht_system_flags": (ctypes.c_int, [_vp]),

@@ -48,6 +48,16 @@ class System:
         self.n, self.M, self.max_terms = nn.value, M.value, mt.value
         self.dense = bool(lib.pht_system_flags(h) & _lib.SYS_DENSE)  # FP64 tensor-core evaluation path
 
+    def homogenize(self, x, log_input: bool = False):
+        """pht_homogenize: affine points x [p, n_eq] (or z = log x) -> y [p, n_eq + 1] on ||y|| = 1."""
+        if not (x.is_cuda and x.dtype == torch.complex128 and x.dim() == 2 and x.shape[1] == self.n - 1
+                and x.is_contiguous()):
+            raise PhtError("x must be a contiguous cuda complex128 tensor [p, n_eq]")
+        y = torch.empty((x.shape[0], self.n), dtype=torch.complex128, device=self._dev())
+        check(self._lib.pht_homogenize(self._h, x.shape[0], _ptr(x), int(bool(log_input)), _ptr(y),
+                                       _stream(self._dev())), "pht_homogenize")
+        return y
+
     def set_solver(self, solver: str = "lu"):
         """pht_system_set_solver: 'lu' (Gauss-Jordan, default) or 'qr' (Householder, P:708-726)."""
         code = {"lu": _lib.SOLVER_LU, "qr": _lib.SOLVER_QR}[solver]

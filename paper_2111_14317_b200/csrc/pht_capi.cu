@@ -588,6 +588,55 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
     return PHT_OK;
 }
 
+// Affine points -> P^n (pht_homogenize): y = (x, 1) / ||(x, 1)||, x = e^z for log input.
+// One thread per point; coordinates scaled by the largest magnitude before the norm.
+__global__ void k_homogenize(int64_t p, int n, const double2 *x, int log_input, double2 *y)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= p) return;
+    const double2 *xq = x + q * n;
+    double lmax = 0.0; // log of the largest |coordinate| (the appended 1 included)
+    for (int j = 0; j < n; ++j) {
+        const double2 v = xq[j];
+        lmax = fmax(lmax, log_input ? v.x : log(hypot(v.x, v.y)));
+    }
+    double s2 = 0.0;
+    double2 *yq = y + q * (n + 1);
+    for (int j = 0; j <= n; ++j) {
+        double2 u;
+        if (j == n) u = make_double2(exp(-lmax), 0.0);
+        else if (log_input) {
+            double sn, cs;
+            sincos(xq[j].y, &sn, &cs);
+            const double m = exp(xq[j].x - lmax);
+            u = make_double2(m * cs, m * sn);
+        } else {
+            const double f = exp(-lmax);
+            u = make_double2(xq[j].x * f, xq[j].y * f);
+        }
+        yq[j] = u;
+        s2 = fma(u.x, u.x, fma(u.y, u.y, s2));
+    }
+    const double f = rsqrt(s2);
+    for (int j = 0; j <= n; ++j) yq[j] = make_double2(yq[j].x * f, yq[j].y * f);
+}
+
+extern "C" int pht_homogenize(const pht_system *s, int64_t p, const double *x, int32_t log_input, double *y,
+                              void *stream)
+{
+    if (!s || !s->proj || p < 0 || (p > 0 && (!x || !y))) return PHT_EINVAL;
+    if (p == 0) return PHT_OK;
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    const int threads = 128;
+    k_homogenize<<<(unsigned)((p + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+        p, s->n - 1, (const double2 *)x, log_input, (double2 *)y);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return PHT_OK;
+}
+
 extern "C" void pht_track_opts_default(pht_track_opts *o)
 {
     if (!o) return;

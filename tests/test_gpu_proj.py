@@ -171,3 +171,15 @@ def test_proj_two_stage_cyclic5(P):
     assert np.max(np.linalg.norm(xg - xo, axis=1) / np.linalg.norm(xo, axis=1)) <= 1e-8
     with pytest.raises(P.PhtError):
         g.track(_cuda(y1), _cuda(np.full(len(y1), PH.TAU0)), log_state=1)
+
+
+def test_homogenize_points(P):
+    sysm = W.cyclic(5, lift_max=20)
+    g = P.System.from_workload(sysm, projective=True)
+    z, _ = W.random_log_points(100, 5, seed=61, rho_max=8.0)
+    y1 = g.homogenize(_cuda(z), log_input=True).cpu().numpy()
+    y2 = g.homogenize(_cuda(np.exp(z)), log_input=False).cpu().numpy()
+    assert np.allclose(np.linalg.norm(y1, axis=1), 1.0, atol=1e-15)
+    x = np.exp(z)
+    assert np.max(np.abs(y1[:, :5] / y1[:, 5:] - x) / np.abs(x)) < 1e-13
+    assert np.max(np.abs(y1 - y2)) < 1e-14
