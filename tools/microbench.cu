@@ -186,6 +186,50 @@ int main()
         double flops = 512.0 * 4 * iters * (double)blocks * (threads / 32);
         printf(", \"dmma_tflops\": %.3f", flops / (ms * 1e-3) / 1e12);
     }
+    // co-issue: DMMA and DFMA kernels on two streams at the same time (only
+    // worth splitting work across the tensor and FP64 pipes if the two overlap)
+    {
+        const int iters = 20000, blocks = sms * 4, threads = 256;
+        cudaStream_t s1, s2;
+        cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+        cudaEvent_t a0, a1;
+        cudaEventCreate(&a0);
+        cudaEventCreate(&a1);
+        float ms_m, ms_f, ms_b;
+        cudaEventRecord(a0, s1);
+        k_dmma<4><<<blocks, threads, 0, s1>>>(d, iters);
+        cudaEventRecord(a1, s1);
+        CK(cudaEventSynchronize(a1));
+        cudaEventElapsedTime(&ms_m, a0, a1);
+        cudaEventRecord(a0, s1);
+        k_dfma<8><<<blocks, threads, 0, s1>>>(d, iters, 1.0000001, 1e-9);
+        cudaEventRecord(a1, s1);
+        CK(cudaEventSynchronize(a1));
+        cudaEventElapsedTime(&ms_f, a0, a1);
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(a0, 0);
+        cudaEvent_t j0;
+        cudaEventCreate(&j0);
+        cudaEventRecord(j0, 0);
+        cudaStreamWaitEvent(s1, j0, 0);
+        cudaStreamWaitEvent(s2, j0, 0);
+        k_dmma<4><<<blocks / 2, threads, 0, s1>>>(d, iters);
+        k_dfma<8><<<blocks / 2, threads, 0, s2>>>(d, iters, 1.0000001, 1e-9);
+        cudaEvent_t e1s, e2s;
+        cudaEventCreate(&e1s);
+        cudaEventCreate(&e2s);
+        cudaEventRecord(e1s, s1);
+        cudaEventRecord(e2s, s2);
+        cudaStreamWaitEvent(0, e1s, 0);
+        cudaStreamWaitEvent(0, e2s, 0);
+        cudaEventRecord(a1, 0);
+        CK(cudaEventSynchronize(a1));
+        cudaEventElapsedTime(&ms_b, a0, a1);
+        // half of each workload together vs the sum of the halves alone (ms_m/2 + ms_f/2)
+        printf(", \"coissue\": {\"dmma_ms\": %.3f, \"dfma_ms\": %.3f, \"half_each_concurrent_ms\": %.3f, "
+               "\"half_each_serial_ms\": %.3f}", ms_m, ms_f, ms_b, 0.5 * (ms_m + ms_f));
+    }
     printf("}\n");
     return 0;
 }
