@@ -193,6 +193,70 @@ def cpu_baseline(seconds_target=12.0):
                       f"{dt:.1f} s on {cores} threads"}
 
 
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the B200 nominal."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 7700.0, "B200_PROFILING.md nominal HBM3e"
+
+
+EVAL_CONFIGS = [("cyclic-10", 1 << 21, "BASELINE.json configs[2]: cyclic-10 batched H, dH/dx, dH/dt"),
+                ("random-20x50", 1 << 18, "BASELINE.json configs[3]: random dense Laurent n=20, 50 terms/eq "
+                                          "(FP64 tensor-core DMMA evaluation)")]
+
+
+def evaluation_section(world, rank, dev, reps=5):
+    """Standalone batched evaluation (pht_evaluate: H, Jx, Jt written to HBM) with both roofline
+    fractions: HBM bytes moved (x, t in; H, Jx, Jt out) vs the measured copy bandwidth, and the
+    algorithmic FP64 flops (evaluation part) vs the FP64 peak."""
+    import torch
+    import torch.distributed as dist
+    import paper_2111_14317_b200 as P
+    import workloads as W
+    out = {}
+    peak_bw, bw_src = hbm_peak_gbs()
+    for name, Pn, label in EVAL_CONFIGS:
+        sysm = W.cyclic(10, lift_max=LIFT_MAX) if name == "cyclic-10" else W.random_dense(20, 50)
+        g = P.System.from_workload(sysm, device=dev.index)
+        x, t, _ = W.random_points(Pn, sysm.n, seed=2000 + rank, rho_max=0.5 if sysm.n > 12 else 1.0)
+        xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
+        n = sysm.n
+        H = torch.empty((Pn, n), dtype=torch.complex128, device=dev)
+        J = torch.empty((Pn, n, n), dtype=torch.complex128, device=dev)
+        Jt = torch.empty((Pn, n), dtype=torch.complex128, device=dev)
+        st = torch.empty(Pn, dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            g.evaluate(xd, td, out=(H, J, Jt, st))
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.evaluate(xd, td, out=(H, J, Jt, st))
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = float(ms.item())
+        byts = Pn * (16 * n + 8 + 16 * (n + n * n + n) + 1)
+        fl = algorithmic_flops_per_eval(sysm)["eval"] * Pn
+        out[name] = {"workload": label, "points_per_gpu": Pn, "ms_per_launch": ms,
+                     "points_per_s": world * Pn / (ms * 1e-3),
+                     "hbm": {"achieved_gbs": byts / (ms * 1e-3) / 1e9, "peak_gbs": peak_bw, "peak_basis": bw_src,
+                             "frac": byts / (ms * 1e-3) / 1e9 / peak_bw, "bytes_per_point": byts // Pn},
+                     "fp64": {"achieved_tflops": fl / (ms * 1e-3) / 1e12, "peak_tflops": fp64_peak_tflops(1965.0),
+                              "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak_tflops(1965.0),
+                              "flops_per_point": fl / Pn},
+                     "path": "FP64 tensor cores (DMMA)" if g.dense else "scalar FP64 kernel"}
+        del g, xd, td, H, J, Jt, st
+    return out
+
+
 TRACK_CONFIGS = [("katsura-10", 10_000, "BASELINE.json configs[1]: katsura-10 full path tracking"),
                  ("noon-10", 10_000, "BASELINE.json configs[4]: noon-10 (large liftings) tracked to t=1 + endpoint gather"),
                  ("cyclic-10", 1_000_000, "BASELINE.json configs[2]: cyclic-10 predictor-corrector tracking, sharded")]
@@ -315,6 +379,8 @@ def main():
     ap.add_argument("--ref-points", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-evaluation", dest="evaluation", action="store_false",
+                    help="skip the standalone-evaluation section")
     ap.add_argument("--solver", default="lu", choices=["lu", "qr"], help="direction solver (pht_system_set_solver)")
     ap.add_argument("--specialize", action="store_true", help="system-specialised kernels (pht_system_specialize)")
     ap.add_argument("--tracking", default="katsura-10,noon-10,cyclic-10",
@@ -399,6 +465,7 @@ def main():
 
     tracking = tracking_section(world, rank, dev, [t for t in args.tracking.split(",") if t]) \
         if args.tracking else {}
+    evaluation = evaluation_section(world, rank, dev) if args.evaluation else {}
 
     if rank == 0:
         clocks = clk.summary() or {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
@@ -427,6 +494,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clocks,
             "tracking": tracking,
+            "evaluation": evaluation,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()

@@ -105,15 +105,23 @@ class System:
             raise PhtError("t/tau must be a contiguous cuda float64 tensor [p]")
 
     def evaluate(self, x, t, scaled: bool = False, out=None):
-        """H, Jx, Jt (+ row_exp2 if scaled), status at points x [p,n], t [p] (pht_evaluate)."""
+        """H, Jx, Jt (+ row_exp2 if scaled), status at points x [p,n], t [p] (pht_evaluate).
+        out: optional preallocated (H, Jx, Jt, status) device tensors (no allocation per call)."""
         self._check_pts(x, t)
         p, n = x.shape
         d = self._dev()
-        H = torch.empty((p, n), dtype=torch.complex128, device=d)
-        Jx = torch.empty((p, n, n), dtype=torch.complex128, device=d)
-        Jt = torch.empty((p, n), dtype=torch.complex128, device=d)
+        if out is not None:
+            H, Jx, Jt, st = out
+            for a, shape, dt in ((H, (p, n), torch.complex128), (Jx, (p, n, n), torch.complex128),
+                                 (Jt, (p, n), torch.complex128), (st, (p,), torch.uint8)):
+                if not (a.is_cuda and a.dtype == dt and tuple(a.shape) == shape and a.is_contiguous()):
+                    raise PhtError("out tensors must be contiguous cuda (H [p,n], Jx [p,n,n], Jt [p,n] c128, status [p] u8)")
+        else:
+            H = torch.empty((p, n), dtype=torch.complex128, device=d)
+            Jx = torch.empty((p, n, n), dtype=torch.complex128, device=d)
+            Jt = torch.empty((p, n), dtype=torch.complex128, device=d)
+            st = torch.empty(p, dtype=torch.uint8, device=d)
         e2 = torch.empty((p, n), dtype=torch.int32, device=d) if scaled else None
-        st = torch.empty(p, dtype=torch.uint8, device=d)
         check(self._lib.pht_evaluate(self._h, p, _ptr(x), _ptr(t), _ptr(H), _ptr(Jx), _ptr(Jt), _ptr(e2),
                                      _ptr(st), _stream(d)), "pht_evaluate")
         return (H, Jx, Jt, e2, st) if scaled else (H, Jx, Jt, st)
