@@ -1,4 +1,4 @@
-"""One pht_evaluate launch on cyclic-10 (for ncu captures of the standalone evaluation kernel)."""
+"""One pht_evaluate launch (for ncu captures): argv[1] = system, PHT_SPEC=1 specialises."""
 import os
 import sys
 
@@ -8,10 +8,16 @@ import torch  # noqa: E402
 import paper_2111_14317_b200 as P  # noqa: E402
 import workloads as W  # noqa: E402
 
-p = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
-sysm = W.cyclic(10, lift_max=100)
+name = sys.argv[1] if len(sys.argv) > 1 else "cyclic-10"
+sysm = {"cyclic-10": lambda: W.cyclic(10, lift_max=100), "random-20x50": lambda: W.random_dense(20, 50),
+        "cyclic-5": lambda: W.cyclic(5)}[name]()
 g = P.System.from_workload(sysm)
-x, t, _ = W.random_points(p, 10, seed=1)
-out = g.evaluate(torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda())
+if os.environ.get("PHT_SPEC") == "1":
+    g.specialize()
+p = 1 << 20 if sysm.n <= 10 else 1 << 17
+x, t, _ = W.random_points(p, sysm.n, seed=1, rho_max=0.5 if sysm.n > 12 else 1.0)
+xd, td = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()
+for _ in range(2):
+    g.evaluate(xd, td)
 torch.cuda.synchronize()
-print("ok", p)
+print("ok")
