@@ -322,7 +322,11 @@ struct GeoS {
     static constexpr int MS = (N * RW) | 1;            // matrix slot stride: odd => conflict-free
     static constexpr int KS = (N + 3) & ~3;            // pivot-key slot per point (16 B aligned)
     // co-resident CTAs per SM: aim at 16 warps (4 per SMSP -> 128 registers per thread)
+#ifdef PHT_GEOS_MINB
+    static constexpr int MINB = N <= 12 ? PHT_GEOS_MINB : 1; // experiments
+#else
     static constexpr int MINB = N <= 12 ? (PHT_RT_SMEM(N) ? (16 / NWARP > 1 ? 16 / NWARP : 1) : 2) : 1;
+#endif
 };
 
 // Geometry of the system-specialised kernels (pht_jit.cu): the generated row code is
@@ -660,6 +664,8 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
     double2 myrcp = make_double2(0.0, 0.0);
 #pragma unroll
     for (int j = 0; j < N; ++j) {
+        const double crd = __drcp_rn(fma(a[j].x, a[j].x, a[j].y * a[j].y));
+        const double2 crcp = make_double2(a[j].x * crd, -a[j].y * crd);
         unsigned key = 0u;
         if (!used) key = ((unsigned)__double2hiint(cabs1(a[j])) & ~63u) | (unsigned)(32 - i);
         unsigned kmax = 0u;
@@ -689,17 +695,19 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
             col = j;
         }
         if (me && act) {
+            // the pivot row with the pivot replaced by its reciprocal (computed before the
+            // argmax by every lane for its own candidate: the reciprocal's latency overlaps the
+            // pivot search instead of following the row broadcast)
+            slot[r * RW + j] = crcp;
 #pragma unroll
-            for (int c = j; c < RW; ++c) slot[r * RW + c] = a[c];
+            for (int c = j + 1; c < RW; ++c) slot[r * RW + c] = a[c];
         }
         __syncwarp();
-        const double2 pv = slot[r * RW + j];
-        const double rd = __drcp_rn(fma(pv.x, pv.x, pv.y * pv.y));
-        const double2 rcp = make_double2(pv.x * rd, -pv.y * rd);
+        const double2 rcp = slot[r * RW + j];
         if (me) {
-            myrcp = rcp;
-            const double pa = cabs1(pv);
-            if (!(pa > 1e-14 * rmax) || !isfinite(pa) || !isfinite(rd)) singular = true;
+            myrcp = crcp;
+            const double pa = cabs1(a[j]);
+            if (!(pa > 1e-14 * rmax) || !isfinite(pa) || !isfinite(crd)) singular = true;
         }
         // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row
         double2 l = cmul(a[j], rcp);
