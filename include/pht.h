@@ -270,6 +270,14 @@ typedef struct {
     int32_t pred_log;     /* Euler predictor chart: 0 affine x + h dx/dtau (the paper's form,
                              P:254-259); 1 log chart z + h dz/dtau (exact for the toric paths
                              x ~ e^{tau alpha} y near tau0); -1 (default) = log_state          */
+    double pred_tol;      /* 0      step-size control (reading R14): > 0: after an accepted step the
+                             next step is dtau * clamp(sqrt(pred_tol / e1), shrink, grow), e1 =
+                             size of the first corrector update (the Euler predictor's error,
+                             O(dtau^2)); <= 0 (default): grow by `grow` after `grow_after`
+                             successes (measured faster on the benchmark systems).
+                             A corrector iterate is accepted when its update, or the update
+                             times the observed contraction (quadratic convergence estimate),
+                             is <= newton_tol.                                               */
 } pht_track_opts;
 
 void pht_track_opts_default(pht_track_opts *opts);

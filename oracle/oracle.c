@@ -597,7 +597,7 @@ static double relmax(int n, const double *d, const double *x)
  * Adaptive tracking tau0 -> 0 (step control = DESIGN.md reading R14: the
  * corrector converges when max_j |dN_j|/|x_j| <= newton_tol, a scale-invariant test because
  * polyhedral start points span many orders of magnitude).
- * opt[] = {dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm}
+ * opt[] = {dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm, pred_tol}
  * iopt[] = {K (max corrector iters), grow_after, max_steps, final_iters, pred_log}
  * pred_log: the Euler predictor in the log chart, x exp(h dz/dtau), instead of x + h dx/dtau.
  * stats[q] = {accepted steps, rejected steps, evaluations (solves), final Newton iters}.
@@ -610,6 +610,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
     orc_sys s = {n, off, a, c, w, n};
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
+    const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
     const int pred_log = iopt[4];
 #pragma omp parallel for schedule(dynamic, 1)
@@ -618,6 +619,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
         int succ = 0, st = 0;
+        double nd1 = -1.0; /* first corrector update of the current step */
         if (!isfinite(tq)) {
             status[q] = ORC_PT_NONFINITE;
             for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
@@ -632,6 +634,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             double tt = tq + h;
             if (!s1) {
                 double t = exp(tq), prev = INFINITY;
+                nd1 = -1.0;
                 if (pred_log) { /* Euler in the log chart: x exp(h dz/dtau), dz/dtau = t dE / x */
                     for (int j = 0; j < n; ++j) {
                         cplx xv = load(xq + 2 * j);
@@ -647,7 +650,10 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
                     if (s1) break;
                     double nd = relmax(n, dN, xt);
                     for (int i = 0; i < 2 * n; ++i) xt[i] += dN[i];
-                    if (nd <= newton_tol) { ok = 1; break; }
+                    if (it == 1) nd1 = nd;
+                    /* converged: the update, or the update times the observed contraction
+                     * (quadratic-convergence estimate of the remaining error) <= newton_tol */
+                    if (nd <= newton_tol || (it >= 2 && nd * (nd / prev) <= newton_tol)) { ok = 1; break; }
                     if (it >= 2 && nd > 0.5 * prev) break;
                     prev = nd;
                 }
@@ -656,7 +662,13 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
                 memcpy(xq, xt, sizeof(double) * 2 * n);
                 tq = tt;
                 ++steps;
-                if (++succ == grow_after) { dt = fmin(grow * dt, dtau_max); succ = 0; }
+                if (pred_tol > 0.0) { /* next step from the Euler predictor's error e1 = O(dt^2) */
+                    const double f = nd1 > 0.0 ? fmin(fmax(sqrt(pred_tol / nd1), shrink), grow) : grow;
+                    dt = fmin(f * dt, dtau_max);
+                } else if (++succ == grow_after) {
+                    dt = fmin(grow * dt, dtau_max);
+                    succ = 0;
+                }
             } else {
                 ++rejects;
                 dt *= shrink;
@@ -775,6 +787,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
     orc_sys s = {n, off, a, c, w, n};
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
+    const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
     const int pred_log = iopt[4];
 #pragma omp parallel for schedule(dynamic, 1)
@@ -786,6 +799,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
         int succ = 0, st = 0;
+        double nd1 = -1.0; /* first corrector update of the current step */
         if (!isfinite(tq)) {
             status[q] = ORC_PT_NONFINITE;
             for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
@@ -800,6 +814,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
             double tt = tq + h;
             if (!s1) {
                 double prev = INFINITY;
+                nd1 = -1.0;
                 for (int j = 0; j < n; ++j) xt[j] = xq[j];
                 if (pred_log) /* Euler in the log chart: x exp(h delta_E) */
                     for (int j = 0; j < n; ++j) xt[j] = xmul(xt[j], xnorm(cexp(h * load(dE + 2 * j)), 0));
@@ -811,7 +826,10 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                     if (s1) break;
                     double nd = relmax_d(n, dN);
                     xupdate(n, xt, dN, 1.0);
-                    if (nd <= newton_tol) { ok = 1; break; }
+                    if (it == 1) nd1 = nd;
+                    /* converged: the update, or the update times the observed contraction
+                     * (quadratic-convergence estimate of the remaining error) <= newton_tol */
+                    if (nd <= newton_tol || (it >= 2 && nd * (nd / prev) <= newton_tol)) { ok = 1; break; }
                     if (it >= 2 && nd > 0.5 * prev) break;
                     prev = nd;
                 }
@@ -820,7 +838,13 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                 for (int j = 0; j < n; ++j) xq[j] = xt[j];
                 tq = tt;
                 ++steps;
-                if (++succ == grow_after) { dt = fmin(grow * dt, dtau_max); succ = 0; }
+                if (pred_tol > 0.0) { /* next step from the Euler predictor's error e1 = O(dt^2) */
+                    const double f = nd1 > 0.0 ? fmin(fmax(sqrt(pred_tol / nd1), shrink), grow) : grow;
+                    dt = fmin(f * dt, dtau_max);
+                } else if (++succ == grow_after) {
+                    dt = fmin(grow * dt, dtau_max);
+                    succ = 0;
+                }
             } else {
                 ++rejects;
                 dt *= shrink;
@@ -1024,6 +1048,7 @@ int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c,
     const int m = n + 1;
     const double dtau_init = opt[0], dtau_min = opt[1], dtau_max = opt[2], newton_tol = opt[3];
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
+    const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
@@ -1031,6 +1056,7 @@ int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c,
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
         int succ = 0, st = 0;
+        double nd1 = -1.0; /* first corrector update of the current step */
         if (!isfinite(tq)) {
             status[q] = ORC_PT_NONFINITE;
             for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
@@ -1046,6 +1072,7 @@ int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c,
             double tt = tq + h;
             if (!s1) {
                 double prev = INFINITY;
+                nd1 = -1.0;
                 for (int i = 0; i < 2 * m; ++i) yt[i] = yq[i] + h * E[i];
                 proj_normalize(m, yt);
                 for (int it = 1; it <= K; ++it) {
@@ -1055,7 +1082,10 @@ int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c,
                     double nd = vnorm(m, N); /* ||y~|| = 1 */
                     for (int i = 0; i < 2 * m; ++i) yt[i] += N[i];
                     proj_normalize(m, yt);
-                    if (nd <= newton_tol) { ok = 1; break; }
+                    if (it == 1) nd1 = nd;
+                    /* converged: the update, or the update times the observed contraction
+                     * (quadratic-convergence estimate of the remaining error) <= newton_tol */
+                    if (nd <= newton_tol || (it >= 2 && nd * (nd / prev) <= newton_tol)) { ok = 1; break; }
                     if (it >= 2 && nd > 0.5 * prev) break;
                     prev = nd;
                 }
@@ -1064,7 +1094,13 @@ int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c,
                 memcpy(yq, yt, sizeof(double) * 2 * m);
                 tq = tt;
                 ++steps;
-                if (++succ == grow_after) { dt = fmin(grow * dt, dtau_max); succ = 0; }
+                if (pred_tol > 0.0) { /* next step from the Euler predictor's error e1 = O(dt^2) */
+                    const double f = nd1 > 0.0 ? fmin(fmax(sqrt(pred_tol / nd1), shrink), grow) : grow;
+                    dt = fmin(f * dt, dtau_max);
+                } else if (++succ == grow_after) {
+                    dt = fmin(grow * dt, dtau_max);
+                    succ = 0;
+                }
             } else {
                 ++rejects;
                 dt *= shrink;

@@ -80,6 +80,7 @@ struct TrackOpts {
     int K, grow_after, max_steps, final_iters;
     int log_state; // state arrays hold z = log x instead of x
     int pred_log;  // Euler predictor in the log chart: z + h dz/dtau (x exp(h dz/dtau))
+    double pred_tol; // step control from the first corrector update (<= 0: grow_after rule)
 };
 struct TrackArgs {
     int64_t P;
@@ -1053,7 +1054,7 @@ struct TrackSmem {
     double2 xt[N][Geo<N>::WL + 1];   // trial point
     double2 dd[N][Geo<N>::WL + 1];   // direction of this iteration (delta_E or delta_N, log coords)
     double nd2[N][Geo<N>::WL + 1];   // |dx_j / x_j|^2 of this iteration
-    double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL];
+    double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL], nd1[Geo<N>::WL];
     long long path[Geo<N>::WL], steps[Geo<N>::WL], rej[Geo<N>::WL], evals[Geo<N>::WL], fin[Geo<N>::WL];
     int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL], cell[Geo<N>::WL];
     int acc[Geo<N>::WL];         // this iteration: 1 accept x~ -> x
@@ -1278,11 +1279,21 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                     double nd = 0.0; // max_j |dx_j| / |x_j| (componentwise relative, reading R14)
                     for (int j = 0; j < N; ++j) nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
                     nd = sqrt(nd);      // projective: ||dy|| (||y|| = 1, reading R29)
-                    if (nd <= o.newton_tol) {
+                    if (T.it[qq] == 1) T.nd1[qq] = nd;
+                    // converged: the update, or the update times the observed contraction (the
+                    // quadratic-convergence estimate of the remaining error), <= newton_tol (R14)
+                    if (nd <= o.newton_tol || (T.it[qq] >= 2 && nd * (nd / T.prev[qq]) <= o.newton_tol)) {
                         T.acc[qq] = 1;
                         T.tau_a[qq] = T.tau_t[qq];
                         T.steps[qq] += 1;
-                        if (++T.succ[qq] == o.grow_after) { T.dt[qq] = fmin(o.grow * T.dt[qq], o.dtau_max); T.succ[qq] = 0; }
+                        if (o.pred_tol > 0.0) { // next step from the Euler predictor's error, O(dtau^2)
+                            const double e1 = T.nd1[qq];
+                            const double f = (e1 > 0.0) ? fmin(fmax(sqrt(o.pred_tol / e1), o.shrink), o.grow) : o.grow;
+                            T.dt[qq] = fmin(f * T.dt[qq], o.dtau_max);
+                        } else if (++T.succ[qq] == o.grow_after) {
+                            T.dt[qq] = fmin(o.grow * T.dt[qq], o.dtau_max);
+                            T.succ[qq] = 0;
+                        }
                         T.phase[qq] = (T.tau_a[qq] < 0.0) ? PH_PREDICT : PH_FINAL;
                         if (T.phase[qq] == PH_PREDICT && T.steps[qq] == o.max_steps) finish = 16; // MAX_STEPS
                     } else if ((T.it[qq] >= 2 && nd > 0.5 * T.prev[qq]) || T.it[qq] >= o.K) {

@@ -51,6 +51,7 @@ for item in which:
     stats = stats.cpu().numpy()
     out.update(paths=len(z), ms=ms, paths_per_s=len(z) / ms * 1e3, status=np.bincount(st, minlength=33)[[0, 2, 4, 8, 16, 32]].tolist(),
                steps_mean=float(stats[:, 0].mean()), steps_max=int(stats[:, 0].max()), evals_total=int(stats[:, 2].sum()),
+               rejects_mean=float(stats[:, 1].mean()), final_mean=float(stats[:, 3].mean()),
                evals_per_s=float(stats[:, 2].sum() / ms * 1e3), start_prep_s=prep,
                max_abs_re_z0=float(np.abs(z.real).max()), tau0_min=float(tau0.min()))
     out["opts"] = OPTS
