@@ -507,7 +507,11 @@ struct RowAcc {
 };
 
 #ifdef PHT_JIT
-// system-specialised rows: defined by the generated source (pht_jit.cu) after this header
+// system-specialised rows: defined by the generated source (pht_jit.cu) after this header.
+// jit_row_core: row k of the point whose (rho, vartheta) column is rt[j * ST].
+template <int N>
+__device__ void jit_row_core(int k, const double2 *rt, int ST, double tau, const double *etab, const double2 *ctab,
+                             double2 (&row)[N + 2], int &e, const double *wq);
 template <int N>
 __device__ void jit_row(const DevSys &S, const Smem<N> &sm, int k, int q, double2 (&row)[N + 2], int &e,
                         const double *wq);
@@ -1036,6 +1040,104 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
     }
 }
 
+
+#ifdef PHT_JIT
+// ---------------------------------------------------------------------------------------
+// Specialised evaluation, one point per thread (pht_evaluate / pht_evaluate_log after
+// pht_system_specialize).  No solve follows, so no per-point matrix tile is needed: each thread
+// runs stage 1 for its point, then the generated rows of all equations in sequence and writes
+// every row straight out.  All warps walk the same equation stream (instruction-cache
+// friendly, unlike the warp-per-equation layout the fused kernels need).
+#ifndef PHT_EVALP_T
+#define PHT_EVALP_T 128
+#endif
+template <int N>
+struct SmemE {
+    double exptab[TAB_E];
+    double2 cistab[TAB_C];
+    double2 rt[N][PHT_EVALP_T + 1];  // (rho, vartheta) columns, one per thread
+    double2 inv[N][PHT_EVALP_T + 1]; // 1/x (EVAL_X epilogue): off the registers live across the rows
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(PHT_EVALP_T, 4) k_evalp(const DevSys S, const Args A)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmemE<N> &sm = *reinterpret_cast<SmemE<N> *>(smem_raw);
+    const int tid = threadIdx.x;
+    load_tables(S, sm.exptab, sm.cistab, tid, PHT_EVALP_T);
+    const int64_t q = (int64_t)blockIdx.x * PHT_EVALP_T + tid;
+    const bool live = q < A.P;
+    int st = 0;
+    double tau = 0.0, tinv = 1.0;
+    {
+        double tv = live ? A.tin[q] : (MODE == MODE_EVAL_Z ? 0.0 : 1.0);
+        if (MODE == MODE_EVAL_Z) {
+            if (!isfinite(tv)) { st |= PT_NONFINITE; tv = 0.0; }
+            tau = tv;
+        } else {
+            if (!(tv > 0.0) || !isfinite(tv)) { st |= PT_NONFINITE; tv = 1.0; }
+            tau = log(tv);
+            tinv = 1.0 / tv;
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double2 v = live ? A.xin[q * N + j] : make_double2(MODE == MODE_EVAL_Z ? 0.0 : 1.0, 0.0);
+            double rho, th;
+            if (MODE == MODE_EVAL_Z) {
+                if (!(isfinite(v.x) && isfinite(v.y))) { st |= PT_NONFINITE; rho = 0.0; th = 0.0; }
+                else {
+                    rho = v.x;
+                    const double kq = rint(v.y * INV_2PI);
+                    th = fma(-kq, TWO_PI_LO, fma(-kq, TWO_PI_HI, v.y));
+                }
+            } else {
+                double2 iv;
+                log_split(v, rho, th, iv, st);
+                sm.inv[j][tid] = iv;
+            }
+            sm.rt[j][tid] = make_double2(rho, th);
+        }
+    }
+    __syncthreads(); // the tables (each rt column is private to its thread)
+    const bool scaled = A.rexp != nullptr;
+    for (int k = 0; k < N; ++k) {
+        double2 row[N + 2];
+        int e = 0;
+        if (S.proj && k == N - 1) { // bordering row y^* (see eval_row)
+#pragma unroll
+            for (int j = 0; j < N; ++j) row[j] = make_double2(exp(2.0 * sm.rt[j][tid].x), 0.0);
+            row[N] = make_double2(0.0, 0.0);
+            row[N + 1] = make_double2(0.0, 0.0);
+        } else {
+            jit_row_core<N>(k, &sm.rt[0][tid], PHT_EVALP_T + 1, tau, sm.exptab, sm.cistab, row, e, nullptr);
+        }
+        if (MODE == MODE_EVAL_X) {
+            row[N] = make_double2(row[N].x * tinv, row[N].y * tinv);
+#pragma unroll
+            for (int j = 0; j < N; ++j) row[j] = cmul(row[j], sm.inv[j][tid]);
+        }
+        if (!scaled && e != 0) {
+#pragma unroll
+            for (int c = 0; c < N + 2; ++c) row[c] = make_double2(scalbn(row[c].x, e), scalbn(row[c].y, e));
+        }
+        bool fin = true;
+#pragma unroll
+        for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(row[c].x) && isfinite(row[c].y);
+        if (!fin) st |= PT_NONFINITE;
+        if (live) {
+            if (A.J) {
+#pragma unroll
+                for (int j = 0; j < N; ++j) A.J[(q * N + k) * N + j] = row[j];
+            }
+            if (A.Jt) A.Jt[q * N + k] = row[N];
+            if (A.H) A.H[q * N + k] = row[N + 1];
+            if (scaled) A.rexp[q * N + k] = e;
+        }
+    }
+    if (live && A.status) A.status[q] = (uint8_t)st;
+}
+#endif
 
 // ---------------------------------------------------------------------------------------
 // a6: persistent device tracker (SURVEY §8(a) a6, step control = DESIGN.md reading R14).
