@@ -49,6 +49,7 @@ struct pht_system {
     int dense = 0;
     double *d_b2phi = nullptr, *d_b2th = nullptr, *d_b4 = nullptr;
     int *d_ntoff = nullptr;
+    int max_ntk = 0; // most n-tiles (8 terms) of one equation: size of the staged B tiles
     // packed tables on the host (input of the code generator, pht_system_specialize)
     std::vector<double> h_rec;
     std::vector<int> h_off;
@@ -210,7 +211,10 @@ static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const in
         if (want) {
             const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;
             std::vector<int> ntoff(n + 1, 0);
-            for (int k = 0; k < n; ++k) ntoff[k + 1] = ntoff[k] + (int)((off[k + 1] - off[k] + 7) / 8);
+            for (int k = 0; k < n; ++k) {
+                ntoff[k + 1] = ntoff[k] + (int)((off[k + 1] - off[k] + 7) / 8);
+                s->max_ntk = std::max(s->max_ntk, ntoff[k + 1] - ntoff[k]);
+            }
             const int NT = ntoff[n];
             std::vector<double> b2p((size_t)NT * KS * 32), b2t((size_t)NT * KS * 32), b4((size_t)2 * NT * CT * 32);
             for (int k = 0; k < n; ++k) {
@@ -435,7 +439,7 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
         return PHT_OK;
     }
     const bool dense = s->dense && evalm;
-    const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff};
+    const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff, s->max_ntk};
     switch (s->n) {
 #define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)

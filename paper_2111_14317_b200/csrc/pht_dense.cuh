@@ -31,7 +31,26 @@ struct DenseSys {
     const double *b2th;    // [sum_k ntk][KS][32]
     const double *b4;      // [sum_k 2*ntk][CT][32]
     const int *ntile_off;  // [n+1] prefix sums of ntk (n-tiles of 8 terms per equation)
+    int max_ntk;           // max_k ntk: size of one equation's staged B tiles
 };
+
+// doubles of one equation's B operands staged in shared memory: b2phi, b2th (ntk x KS x 32) and
+// b4 (2 ntk x CT x 32), for ntk = max_ntk
+template <int N>
+__host__ __device__ constexpr int dense_eq_doubles_per_tile()
+{
+    return ((N + 2 + 3) / 4) * 32 * 2 + ((N + 2 + 7) / 8) * 32 * 2;
+}
+
+// 16-byte asynchronous global -> shared copies (LDGSTS), all threads of the CTA
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K)); }
 
 template <int N>
 struct DGeo {
@@ -41,11 +60,20 @@ struct DGeo {
 #ifndef PHT_DENSE_NMT
 #define PHT_DENSE_NMT 1
 #endif
-#ifndef PHT_DENSE_WARPS
-#define PHT_DENSE_WARPS 4
+    // measured (profiles/r01_dense_tuning.txt): n <= 15: 8 warps share a double-buffered staged B
+    // (prefetch of equation k+1 during k); n >= 16 (32 KB of B per equation): 4 warps, one buffer
+    // (shared memory then still allows 3 CTAs per SM)
+#ifdef PHT_DENSE_WARPS
+    static constexpr int WARPS = PHT_DENSE_WARPS;
+#else
+    static constexpr int WARPS = N >= 16 ? 4 : 8;
+#endif
+#ifdef PHT_DENSE_NBUF
+    static constexpr int NBUF = PHT_DENSE_NBUF;
+#else
+    static constexpr int NBUF = N >= 16 ? 1 : 2;
 #endif
     static constexpr int NMT = PHT_DENSE_NMT;     // M-tiles (8 points) per warp
-    static constexpr int WARPS = PHT_DENSE_WARPS;
     static constexpr int PTS = WARPS * NMT * 8; // points per CTA
 };
 
@@ -137,9 +165,43 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
         }
     }
     const bool scaled = A.rexp != nullptr;
+    // B operands of equation k are staged in shared memory (double-buffered, cp.async): the
+    // warps of the CTA share them instead of each streaming them from L2 (ncu: long-scoreboard
+    // stalls on the B loads were the first limiter)
+    double *bbuf = reinterpret_cast<double *>(smem_raw + ((sizeof(DenseSmem<N>) + 15) & ~(size_t)15));
+    const int EQB = D.max_ntk * dense_eq_doubles_per_tile<N>();
+    auto stage = [&](int k, int buf) {
+        const int t0 = __ldg(D.ntile_off + k), nt = __ldg(D.ntile_off + k + 1) - t0;
+        double *dst = bbuf + (size_t)buf * EQB;
+        const int n2 = nt * KS * 32, n4 = 2 * nt * CT * 32; // doubles per segment (multiples of 32)
+        const double *s0 = D.b2phi + (size_t)t0 * KS * 32, *s1 = D.b2th + (size_t)t0 * KS * 32,
+                     *s2 = D.b4 + (size_t)t0 * 2 * CT * 32;
+        for (int u = tid; u < n2 / 2; u += G::WARPS * 32) {
+            cp_async16(dst + 2 * u, s0 + 2 * u);
+            cp_async16(dst + n2 + 2 * u, s1 + 2 * u);
+        }
+        for (int u = tid; u < n4 / 2; u += G::WARPS * 32) cp_async16(dst + 2 * n2 + 2 * u, s2 + 2 * u);
+    };
+    constexpr int NB = G::NBUF;
+    if (NB == 2) {
+        stage(0, 0);
+        cp_async_commit();
+    }
 
     for (int k = 0; k < N; ++k) {
         const int nt0 = __ldg(D.ntile_off + k), nt1 = __ldg(D.ntile_off + k + 1);
+        if (NB == 2) {
+            if (k + 1 < N) stage(k + 1, (k + 1) & 1);
+            cp_async_commit();
+            cp_async_wait<1>(); // equation k's tiles have landed (this thread's copies)
+        } else {
+            stage(k, 0);
+            cp_async_commit();
+            cp_async_wait<0>();
+        }
+        __syncthreads(); // ... and everyone else's
+        const double *bk = bbuf + (size_t)(NB == 2 ? (k & 1) : 0) * EQB;
+        const int n2k = (nt1 - nt0) * KS * 32;
         // stage-4 accumulators [m][ct][re/im][2]
         double acc[NMT][CT][2][2];
         double ed[NMT], eh[NMT], el[NMT]; // per-point row exponent (this thread's row g)
@@ -155,11 +217,11 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
             double ph[NMT][2], th[NMT][2];
 #pragma unroll
             for (int m = 0; m < NMT; ++m) ph[m][0] = ph[m][1] = th[m][0] = th[m][1] = 0.0;
-            const double *bp = D.b2phi + ((size_t)nt * KS) * 32 + lane;
-            const double *bt = D.b2th + ((size_t)nt * KS) * 32 + lane;
+            const double *bp = bk + ((size_t)(nt - nt0) * KS) * 32 + lane;
+            const double *bt = bp + n2k;
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk) {
-                const double vp = __ldg(bp + kk * 32), vt = __ldg(bt + kk * 32);
+                const double vp = bp[kk * 32], vt = bt[kk * 32];
 #pragma unroll
                 for (int m = 0; m < NMT; ++m) {
                     dmma(ph[m][0], ph[m][1], aP[m][kk], vp);
@@ -203,10 +265,10 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
             for (int h = 0; h < 2; ++h) {
                 const int jt = 4 * h + r;              // term of this lane's A element
                 const int src = (lane & ~3) | (jt >> 1); // quad lane holding it
-                const double *b4 = D.b4 + ((size_t)(2 * nt + h) * CT) * 32 + lane;
+                const double *b4 = bk + 2 * n2k + ((size_t)(2 * (nt - nt0) + h) * CT) * 32 + lane;
                 double bv[CT];
 #pragma unroll
-                for (int ct = 0; ct < CT; ++ct) bv[ct] = __ldg(b4 + ct * 32);
+                for (int ct = 0; ct < CT; ++ct) bv[ct] = b4[ct * 32];
 #pragma unroll
                 for (int m = 0; m < NMT; ++m) {
                     const double r0 = __shfl_sync(0xffffffffu, wr[m][0], src);
@@ -251,6 +313,7 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
             if (!fin) atomicOr(&sm.st[q], PT_NONFINITE);
             if (scaled && r == 0 && gq < A.P) A.rexp[gq * N + k] = e;
         }
+        __syncthreads(); // buffer (k & 1) is refilled by the prefetch of equation k + 2
     }
     __syncthreads();
     for (int q = tid; q < PTS; q += G::WARPS * 32)
@@ -263,15 +326,16 @@ cudaError_t launch_dense_mode(const DevSys &S, const DenseSys &D, const Args &A,
     constexpr int PTS = DGeo<N>::PTS;
     const int64_t tiles = (A.P + PTS - 1) / PTS;
     if (tiles == 0) return cudaSuccess;
-    const size_t sb = sizeof(DenseSmem<N>);
-    static std::atomic<unsigned long long> configured{0};
+    const size_t sb = ((sizeof(DenseSmem<N>) + 15) & ~(size_t)15) +
+                      (size_t)DGeo<N>::NBUF * D.max_ntk * dense_eq_doubles_per_tile<N>() * sizeof(double);
+    // the staged B tiles make the size system dependent: set the attribute to the largest seen
+    static std::atomic<size_t> configured_sb[64];
     int dev = 0;
     cudaGetDevice(&dev);
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(configured.load() & bit)) {
+    if (configured_sb[dev & 63].load() < sb) {
         cudaError_t e = cudaFuncSetAttribute(k_dense<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
         if (e != cudaSuccess) return e;
-        configured.fetch_or(bit);
+        configured_sb[dev & 63].store(sb);
     }
     k_dense<N, MODE><<<dim3((unsigned)tiles), dim3(DGeo<N>::WARPS * 32), sb, stream>>>(S, D, A);
     return cudaGetLastError();
