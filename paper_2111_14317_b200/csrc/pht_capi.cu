@@ -563,8 +563,13 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
     if ((e = cudaEventRecord(s->hev0, st)) != cudaSuccess) return cuda_fail(e);
     for (int u = 0; u < PHT_HOST_STREAMS; ++u)
         if ((e = cudaStreamWaitEvent(s->hs[u], s->hev0, 0)) != cudaSuccess) return cuda_fail(e);
-    // chunks: ~1/8 of the batch, at least 32K points (launch + copy latency stay amortised)
-    int64_t chunk = (p + 7) / 8;
+    // chunks: 1/PHT_HOST_CHUNKS of the batch (default 32: measured 8 -> 416, 16 -> 453, 32 -> 471,
+    // 64 -> 453 M evals/s end to end on the bench step), at least 32K points (launch and copy
+    // latency stay amortised); the pipeline fill (first copy-in) and drain (last copy-out) are
+    // one chunk each
+    int nch = 32;
+    if (const char *ev = getenv("PHT_HOST_CHUNKS")) nch = std::max(1, atoi(ev));
+    int64_t chunk = (p + nch - 1) / nch;
     if (chunk < 32768) chunk = 32768;
     int c = 0;
     for (int64_t b = 0; b < p; b += chunk, ++c) {

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-python tools/eval_bench.py > gpurun_out/evald.txt 2>&1
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -q -x -k "dense or evaluate or evaluation" > gpurun_out/dense_tests.log 2>&1; echo "rc=$?" >> gpurun_out/dense_tests.log
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --tracking "" > gpurun_out/ab_bench.json 2> gpurun_out/ab_bench.err
+rm -f gpurun_out/e2e.txt
+for c in 8 16 32 64; do
+  PHT_HOST_CHUNKS=$c python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 5 --tracking "" --no-evaluation > gpurun_out/e2e_$c.json 2>/dev/null
+  echo "$c $(python -c "import json; d=json.load(open('gpurun_out/e2e_$c.json')); print(d['value'], d['e2e']['value'])")" >> gpurun_out/e2e.txt
+done
