@@ -278,6 +278,10 @@ typedef struct {
                              A corrector iterate is accepted when its update, or the update
                              times the observed contraction (quadratic convergence estimate),
                              is <= newton_tol.                                               */
+    int32_t predictor;    /* 0 (default) Euler (the paper's protocol); 1 cubic Hermite
+                             extrapolation in the log chart through the previous and the current
+                             accepted point and their Euler directions (log chart
+                             only, i.e. pred_log = 1: Euler otherwise)                        */
 } pht_track_opts;
 
 void pht_track_opts_default(pht_track_opts *opts);

@@ -790,12 +790,23 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
     const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
     const int pred_log = iopt[4];
+    /* predictor 1: cubic Hermite extrapolation in the log chart through the previous and the
+     * current accepted point and their Euler directions, log chart only */
+    const int hermite = pred_log && iopt[5] == 1;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
         xc xq[64], xt[64];
         double dE[128], dN[128];
+        /* continuous log coordinates of the current, trial and previous accepted points (the
+         * Hermite predictor needs differences of z without branch jumps) */
+        cplx zq[64], zt[64], zp[64], ep[64];
+        int has_prev = 0;
+        double tp = 0.0;
         const double *wr = cellw ? cellw + (size_t)path_cell[q] * off[n] : 0;
-        for (int j = 0; j < n; ++j) xq[j] = xnorm(load(xm + 2 * (q * n + j)), xe[q * n + j]);
+        for (int j = 0; j < n; ++j) {
+            xq[j] = xnorm(load(xm + 2 * (q * n + j)), xe[q * n + j]);
+            zq[j] = clog(xq[j].m) + (double)xq[j].e * 0.69314718055994530942;
+        }
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
         int succ = 0, st = 0;
@@ -816,16 +827,33 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                 double prev = INFINITY;
                 nd1 = -1.0;
                 for (int j = 0; j < n; ++j) xt[j] = xq[j];
-                if (pred_log) /* Euler in the log chart: x exp(h delta_E) */
-                    for (int j = 0; j < n; ++j) xt[j] = xmul(xt[j], xnorm(cexp(h * load(dE + 2 * j)), 0));
-                else
+                if (hermite && has_prev) {
+                    /* p(s) on [tp, tq], s = (tau - tp) / D, evaluated at s = 1 + h / D:
+                     * z~ = h00 z_p + h10 D e_p + h01 z_q + h11 D e_q */
+                    const double D = tq - tp, sv = 1.0 + h / D, s2 = sv * sv, s3 = s2 * sv;
+                    const double h00 = 2 * s3 - 3 * s2 + 1, h10 = s3 - 2 * s2 + sv, h01 = -2 * s3 + 3 * s2,
+                                 h11 = s3 - s2;
+                    for (int j = 0; j < n; ++j) {
+                        const cplx eq = load(dE + 2 * j);
+                        zt[j] = h00 * zp[j] + h10 * D * ep[j] + h01 * zq[j] + h11 * D * eq;
+                        xt[j] = xmul(xt[j], xnorm(cexp(zt[j] - zq[j]), 0));
+                    }
+                } else if (pred_log) { /* Euler in the log chart: x exp(h delta_E) */
+                    for (int j = 0; j < n; ++j) {
+                        xt[j] = xmul(xt[j], xnorm(cexp(h * load(dE + 2 * j)), 0));
+                        zt[j] = zq[j] + h * load(dE + 2 * j);
+                    }
+                } else {
                     xupdate(n, xt, dE, h);
+                }
                 for (int it = 1; it <= K; ++it) {
                     s1 = solve_point_x(&s, xt, tt, wr, 0, dN);
                     ++evals;
                     if (s1) break;
                     double nd = relmax_d(n, dN);
                     xupdate(n, xt, dN, 1.0);
+                    if (pred_log)
+                        for (int j = 0; j < n; ++j) zt[j] += clog(1.0 + load(dN + 2 * j));
                     if (it == 1) nd1 = nd;
                     /* converged: the update, or the update times the observed contraction
                      * (quadratic-convergence estimate of the remaining error) <= newton_tol */
@@ -835,7 +863,11 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                 }
             }
             if (ok) {
-                for (int j = 0; j < n; ++j) xq[j] = xt[j];
+                if (hermite)
+                    for (int j = 0; j < n; ++j) { zp[j] = zq[j]; ep[j] = load(dE + 2 * j); }
+                has_prev = 1;
+                tp = tq;
+                for (int j = 0; j < n; ++j) { xq[j] = xt[j]; zq[j] = zt[j]; }
                 tq = tt;
                 ++steps;
                 if (pred_tol > 0.0) { /* next step from the Euler predictor's error e1 = O(dt^2) */

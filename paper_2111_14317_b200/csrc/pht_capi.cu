@@ -663,6 +663,7 @@ extern "C" void pht_track_opts_default(pht_track_opts *o)
     o->final_iters = 5;
     o->log_state = 0;
     o->pred_log = -1;
+    o->predictor = 0;
     o->pred_tol = 0.0; // classic grow_after rule (measured best, profiles/r01_tracker_control.txt)
 }
 
@@ -704,7 +705,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     A.solver = s->solver;
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
-                         o.pred_log < 0 ? o.log_state : o.pred_log, o.pred_tol};
+                         o.pred_log < 0 ? o.log_state : o.pred_log, o.pred_tol, o.predictor};
     // the specialised tracker only with at least one full wave of paths: its tiles are 2-3x larger
     // than the generic kernel's, so few paths would run on few SMs (measured: 70 paths 4x slower)
     // (PHT_JIT_TRACK=1 forces it: tests)

@@ -81,6 +81,7 @@ struct TrackOpts {
     int log_state; // state arrays hold z = log x instead of x
     int pred_log;  // Euler predictor in the log chart: z + h dz/dtau (x exp(h dz/dtau))
     double pred_tol; // step control from the first corrector update (<= 0: grow_after rule)
+    int predictor;   // 1: cubic Hermite extrapolation in the log chart (pred_log), else Euler
 };
 struct TrackArgs {
     int64_t P;
@@ -1155,8 +1156,12 @@ struct TrackSmem {
     double2 xa[N][Geo<N>::WL + 1];   // accepted point (padded rows: see Smem)
     double2 xt[N][Geo<N>::WL + 1];   // trial point
     double2 dd[N][Geo<N>::WL + 1];   // direction of this iteration (delta_E or delta_N, log coords)
+    double2 zp[N][Geo<N>::WL + 1];   // Hermite predictor: previous accepted point (log chart) ...
+    double2 ep[N][Geo<N>::WL + 1];   // ... and its Euler direction dz/dtau
+    double2 ec[N][Geo<N>::WL + 1];   // Euler direction at the current accepted point
     double nd2[N][Geo<N>::WL + 1];   // |dx_j / x_j|^2 of this iteration
-    double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL], nd1[Geo<N>::WL];
+    double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL], nd1[Geo<N>::WL], tau_p[Geo<N>::WL];
+    int has_prev[Geo<N>::WL];
     long long path[Geo<N>::WL], steps[Geo<N>::WL], rej[Geo<N>::WL], evals[Geo<N>::WL], fin[Geo<N>::WL];
     int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL], cell[Geo<N>::WL];
     int acc[Geo<N>::WL];         // this iteration: 1 accept x~ -> x
@@ -1192,6 +1197,7 @@ __device__ __forceinline__ void trk_pop(TrackSmem<N> &T, const TrackArgs &A, int
         T.steps[q] = T.rej[q] = T.evals[q] = T.fin[q] = 0;
         T.succ[q] = 0;
         T.it[q] = 0;
+        T.has_prev[q] = 0;
         T.phase[q] = (t0 < 0.0) ? PH_PREDICT : PH_FINAL;
     } else {
         T.path[q] = -1;
@@ -1267,7 +1273,13 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
         // (1) write back finished paths, accept trial points, load new paths, select the query
         if (tid < N * PTS) {
             const int qq = tid / N, j = tid % N;
-            if (T.acc[qq]) T.xa[j][qq] = T.xt[j][qq];
+            if (T.acc[qq]) {
+                if (o.predictor == 1) { // Hermite history: the point being replaced and its direction
+                    T.zp[j][qq] = T.xa[j][qq];
+                    T.ep[j][qq] = T.ec[j][qq];
+                }
+                T.xa[j][qq] = T.xt[j][qq];
+            }
             if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
             if (T.refill[qq]) T.xa[j][qq] = A.x[T.path[qq] * N + j];
             const int ph = T.phase[qq];
@@ -1337,8 +1349,19 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 const double2 dl = T.dd[j][qq];
                 if (ph == PH_PREDICT) {
                     const double h = fmin(T.dt[qq], -T.tau_a[qq]);
-                    T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], dl, h)
-                                             : trk_update<N, LOGS>(T.xa[j][qq], dl, h);
+                    if (LOGS && o.pred_log && o.predictor == 1 && T.has_prev[qq]) {
+                        // cubic Hermite through (tau_p, z_p, e_p), (tau_a, z_a, delta_E) at s = 1 + h/D
+                        const double D = T.tau_a[qq] - T.tau_p[qq], sv = 1.0 + h / D, s2 = sv * sv, s3 = s2 * sv;
+                        const double h00 = 2 * s3 - 3 * s2 + 1, h10 = s3 - 2 * s2 + sv, h01 = -2 * s3 + 3 * s2,
+                                     h11 = s3 - s2;
+                        const double2 zp = T.zp[j][qq], ep = T.ep[j][qq], za = T.xa[j][qq];
+                        T.xt[j][qq] = make_double2(h00 * zp.x + h10 * D * ep.x + h01 * za.x + h11 * D * dl.x,
+                                                   h00 * zp.y + h10 * D * ep.y + h01 * za.y + h11 * D * dl.y);
+                    } else {
+                        T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], dl, h)
+                                                 : trk_update<N, LOGS>(T.xa[j][qq], dl, h);
+                    }
+                    T.ec[j][qq] = dl;
                 } else if (ph == PH_CORRECT) {
                     const double2 v = T.xt[j][qq];
                     T.xt[j][qq] = trk_update<N, LOGS>(v, dl, 1.0);
@@ -1386,6 +1409,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                     // quadratic-convergence estimate of the remaining error), <= newton_tol (R14)
                     if (nd <= o.newton_tol || (T.it[qq] >= 2 && nd * (nd / T.prev[qq]) <= o.newton_tol)) {
                         T.acc[qq] = 1;
+                        T.tau_p[qq] = T.tau_a[qq];
+                        T.has_prev[qq] = 1;
                         T.tau_a[qq] = T.tau_t[qq];
                         T.steps[qq] += 1;
                         if (o.pred_tol > 0.0) { // next step from the Euler predictor's error, O(dtau^2)

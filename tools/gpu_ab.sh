@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/e2e.txt
-for c in 8 16 32 64; do
-  PHT_HOST_CHUNKS=$c python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 5 --tracking "" --no-evaluation > gpurun_out/e2e_$c.json 2>/dev/null
-  echo "$c $(python -c "import json; d=json.load(open('gpurun_out/e2e_$c.json')); print(d['value'], d['e2e']['value'])")" >> gpurun_out/e2e.txt
+python -m pytest tests/test_gpu_track.py -q -x > gpurun_out/trk_tests.log 2>&1; echo "rc=$?" >> gpurun_out/trk_tests.log
+rm -f gpurun_out/herm.txt
+for o in '{}' '{"predictor": 1}'; do
+  echo "$o" >> gpurun_out/herm.txt
+  TB_OPTS="$o" python tools/track_bench.py katsura-10:10000 noon-10:10000 cyclic-10:1000000 >> gpurun_out/herm.txt 2>&1
 done
