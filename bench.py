@@ -257,6 +257,75 @@ def evaluation_section(world, rank, dev, reps=5):
     return out
 
 
+# The paper's own protocol: 100 consecutive Euler-Newton steps on p points
+# of cyclic-14 / chandra-24; its V100 times for p = 1000: 0.0355 s / 0.0852 s (context only: other
+# hardware, homogeneous coordinates, host transfers included there).
+PAPER_V100_S = {"cyclic-14": 0.0355, "chandra-24": 0.0852}
+
+
+def paper_protocol_section(dev, P_list=(10, 1000, 100_000)):
+    """100 Euler-Newton steps (pc_step, K = 1) on p points, device resident: a plain loop of launches
+    and the same 100 launches captured once in a CUDA graph and replayed (launch-bound at small p)."""
+    import torch
+    import paper_2111_14317_b200 as P
+    import workloads as W
+    out = {}
+    for name, sysm in (("cyclic-14", W.cyclic(14)), ("chandra-24", W.chandra(24))):
+        g = P.System.from_workload(sysm, device=dev.index)
+        n = sysm.n
+        rows = {}
+        for p in P_list:
+            x, _, tau = W.random_points(p, n, seed=3000, rho_max=0.5, tau_lo=-0.05)
+            xd0, td0 = torch.from_numpy(x).to(dev), torch.from_numpy(tau).to(dev)
+            dt = torch.full((p,), 1e-4, dtype=torch.float64, device=dev)
+            st = torch.empty(p, dtype=torch.uint8, device=dev)
+            dn = torch.empty(p, dtype=torch.float64, device=dev)
+            xd, td = xd0.clone(), td0.clone()
+            for _ in range(3):
+                g.pc_step(xd, td, dt, 1, st, dn)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            xd.copy_(xd0); td.copy_(td0)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            for _ in range(100):
+                g.pc_step(xd, td, dt, 1, st, dn)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            loop_ms = e0.elapsed_time(e1)
+            # CUDA graph of the 100 launches (the C ABI enqueues on torch's current stream, which is
+            # the capture stream inside torch.cuda.graph)
+            graph = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                g.pc_step(xd, td, dt, 1, st, dn)
+            torch.cuda.current_stream(dev).wait_stream(s)
+            with torch.cuda.graph(graph):
+                for _ in range(100):
+                    g.pc_step(xd, td, dt, 1, st, dn)
+            xd.copy_(xd0); td.copy_(td0)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+            xd.copy_(xd0); td.copy_(td0)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            graph.replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            graph_ms = e0.elapsed_time(e1)
+            row = {"loop_s": loop_ms * 1e-3, "graph_s": graph_ms * 1e-3,
+                   "point_steps_per_s": 100 * p / (min(loop_ms, graph_ms) * 1e-3)}
+            if p == 1000:
+                row["paper_v100_s"] = PAPER_V100_S[name]
+                row["speedup_vs_paper_v100"] = PAPER_V100_S[name] / (min(loop_ms, graph_ms) * 1e-3)
+            rows[str(p)] = row
+            del graph
+        out[name] = {"workload": f"{name}: 100 Euler-Newton steps (P:911-921), affine coordinates, "
+                                 "points U(|x|=e^[-0.5,0.5]), tau in [-0.05,0], dtau 1e-4",
+                     "terms": sysm.M, "points": rows}
+    return out
+
+
 TRACK_CONFIGS = [("katsura-10", 10_000, "BASELINE.json configs[1]: katsura-10 full path tracking"),
                  ("noon-10", 10_000, "BASELINE.json configs[4]: noon-10 (large liftings) tracked to t=1 + endpoint gather"),
                  ("cyclic-10", 1_000_000, "BASELINE.json configs[2]: cyclic-10 predictor-corrector tracking, sharded")]
@@ -381,6 +450,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-evaluation", dest="evaluation", action="store_false",
                     help="skip the standalone-evaluation section")
+    ap.add_argument("--no-paper-protocol", dest="paper_protocol", action="store_false",
+                    help="skip the paper-protocol (100 Euler-Newton steps, cyclic-14 / chandra-24) section")
     ap.add_argument("--solver", default="lu", choices=["lu", "qr"], help="direction solver (pht_system_set_solver)")
     ap.add_argument("--specialize", action="store_true", help="system-specialised kernels (pht_system_specialize)")
     ap.add_argument("--tracking", default="katsura-10,noon-10,cyclic-10",
@@ -466,6 +537,7 @@ def main():
     tracking = tracking_section(world, rank, dev, [t for t in args.tracking.split(",") if t]) \
         if args.tracking else {}
     evaluation = evaluation_section(world, rank, dev) if args.evaluation else {}
+    paper = paper_protocol_section(dev) if (args.paper_protocol and rank == 0) else {}
 
     if rank == 0:
         clocks = clk.summary() or {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
@@ -495,6 +567,7 @@ def main():
             "clocks": clocks,
             "tracking": tracking,
             "evaluation": evaluation,
+            "paper_protocol": paper,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_edges.py -q > gpurun_out/edge_tests.log 2>&1; echo "rc=$?" >> gpurun_out/edge_tests.log
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 --tracking "" --no-evaluation > gpurun_out/ab_bench.json 2> gpurun_out/ab_bench.err
