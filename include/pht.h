@@ -133,8 +133,10 @@ int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative ph
  * benchmark systems; images are cached per process by generated source).  Calling it again with
  * a subset of the compiled kernels is a no-op.  The tracker uses the specialised kernel only
  * when the batch fills at least one wave of its (larger) tiles; env PHT_JIT_TRACK=1 forces it.
- * Returns PHT_OK, PHT_EJIT (NVRTC failed: log in pht_last_cuda_error), PHT_ECUDA (load failed)
- * or PHT_EINVAL.  Not thread-safe against concurrent calls on the same handle.
+ * Returns PHT_OK, PHT_EJIT (NVRTC failed: log in pht_last_cuda_error), PHT_ECUDA (load failed),
+ * PHT_EUNSUPPORTED (the generated code would exceed sum_terms (nnz(a) + 8) > 8000 units, e.g.
+ * random dense 20 x 50: minutes of compile time and instruction-cache bound; such systems keep
+ * the generic and FP64 tensor-core kernels) or PHT_EINVAL.
  */
 #define PHT_SPEC_EVAL 1
 #define PHT_SPEC_STEP 2

@@ -338,11 +338,27 @@ extern "C" int pht_system_set_solver(pht_system *s, int32_t solver)
 // System-specialised kernels (pht_jit.cu): generate, compile (NVRTC, sm_100a), load.
 static thread_local std::string g_jit_log;
 
+// Size of the straight-line code a system would generate: sum over terms of (nonzero exponents
+// + 8).  Above the limit the compile takes minutes and the code overflows the instruction caches
+// (random dense n = 20 x 50 terms: ~24,000 units, 288 s of NVRTC for the step kernels).
+static const int64_t kJitCodeLimit = 8000;
+static int64_t jit_code_units(int n, const std::vector<double> &rec, const std::vector<int> &off)
+{
+    const int RS = pht::rec_stride(n);
+    int64_t u = 0;
+    for (int i = 0; i < off.back(); ++i) {
+        u += 8;
+        for (int j = 0; j < n; ++j) u += rec[(size_t)i * RS + j] != 0.0;
+    }
+    return u;
+}
+
 extern "C" int pht_system_specialize(pht_system *s, int32_t what)
 {
     if (!s) return PHT_EINVAL;
     if (what == 0) what = PHT_SPEC_ALL;
     if (what & ~PHT_SPEC_ALL) return PHT_EINVAL;
+    if (jit_code_units(s->n, s->h_rec, s->h_off) > kJitCodeLimit) return PHT_EUNSUPPORTED;
     std::lock_guard<std::mutex> lk(s->jit_mu);
     if (s->jit && (pht::jit_what(s->jit) & (unsigned)what) == (unsigned)what) return PHT_OK;
     const std::string src = pht::jit_source(s->n, s->h_rec, s->h_off);

@@ -180,3 +180,16 @@ def test_specialize_subsets_and_flags(P):
     assert np.array_equal(dE.cpu().numpy(), dE0.cpu().numpy())
     with pytest.raises(P.PhtError):
         g.specialize(64)
+
+
+def test_specialize_refuses_oversized_code(P):
+    """Random dense 20 x 50 terms would generate ~24,000 code units (minutes of NVRTC, i-cache
+    bound): PHT_EUNSUPPORTED, and the handle keeps working on the generic / DMMA kernels."""
+    sysm = W.random_dense(20, 50)
+    g = P.System.from_workload(sysm)
+    with pytest.raises(P.PhtError, match="-8"):
+        g.specialize()
+    assert not g.specialized
+    x, t, _ = W.random_points(16, 20, seed=1, rho_max=0.5)
+    H, J, Jt, st = g.evaluate(_cuda(x), _cuda(t))
+    assert np.all(st.cpu().numpy() == 0)
