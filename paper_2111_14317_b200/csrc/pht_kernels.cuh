@@ -952,11 +952,17 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
 
     // DIRS and STEP: evaluation (W) -> shared-memory tile -> warp-level solve (L).
     const int iters = (MODE == MODE_STEP) ? A.K + 1 : 1;
+    // affine step: the apply phase below also computes (rho, vartheta) of each updated coordinate,
+    // so stage 1 (and its barrier) runs only once; projective points are renormalised after the
+    // apply phase, so they take the stage-1 pass every iteration
+    const bool fused_log = (MODE == MODE_STEP) && !S.proj;
     for (int it = 0; it < iters; ++it) {
-        stage1<N, MODE>(sm, tid);
-        if (tid < WL && tid >= PTS)
-            for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
-        __syncthreads();
+        if (it == 0 || !fused_log) {
+            stage1<N, MODE>(sm, tid);
+            if (tid < WL && tid >= PTS)
+                for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
+            __syncthreads();
+        }
         {
             if (k < N) {
                 double2 row[N + 2];
@@ -966,6 +972,10 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
             }
         }
         __syncthreads();
+        // tau~ = tau + dtau for the Newton evaluations; the solve does not read tau, and the
+        // barrier after it orders this before the next evaluation
+        if (MODE == MODE_STEP && it == 0 && tid < PTS)
+            sm.tau[tid] += (base + tid < A.P) ? A.dtau[base + tid] : 0.0;
         auto apply = [&](int col, int qq, double2 dE, double2 dN, bool sing) {
             if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
             const double2 xv = sm.xs[col][qq];
@@ -975,16 +985,28 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
                 const double ti = sm.tinv[qq];
                 sm.inv[col][qq] = make_double2(de.x * ti, de.y * ti);
                 sm.out2[col][qq] = dn;
-            } else if (it == 0) {
-                // Euler: dx/dtau = x (.) delta_E  ->  x~ = x + h x delta_E
-                const double h = (base + qq < A.P) ? A.dtau[base + qq] : 0.0;
-                const double2 d = cmul(xv, dE);
-                sm.xs[col][qq] = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
             } else {
-                // Newton: x~ = x~ + x~ (.) delta_N
-                const double2 d = cmul(xv, dN);
-                sm.xs[col][qq] = make_double2(xv.x + d.x, xv.y + d.y);
-                sm.dn2[col][qq] = fma(d.x, d.x, d.y * d.y);
+                double2 xn;
+                if (it == 0) {
+                    // Euler: dx/dtau = x (.) delta_E  ->  x~ = x + h x delta_E
+                    const double h = (base + qq < A.P) ? A.dtau[base + qq] : 0.0;
+                    const double2 d = cmul(xv, dE);
+                    xn = make_double2(fma(h, d.x, xv.x), fma(h, d.y, xv.y));
+                } else {
+                    // Newton: x~ = x~ + x~ (.) delta_N
+                    const double2 d = cmul(xv, dN);
+                    xn = make_double2(xv.x + d.x, xv.y + d.y);
+                    sm.dn2[col][qq] = fma(d.x, d.x, d.y * d.y);
+                }
+                sm.xs[col][qq] = xn;
+                if (fused_log && it + 1 < iters) { // stage 1 of the next evaluation, for this coordinate
+                    double rho, th;
+                    double2 iv;
+                    int st = 0;
+                    log_split(xn, rho, th, iv, st);
+                    sm.rt[col][qq] = make_double2(rho, th);
+                    if (st) atomicOr(&sm.st[qq], st);
+                }
             }
         };
         if (A.solver == SOLVER_QR) {
@@ -1010,8 +1032,6 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
             if (tid < PTS) proj_normalize<N>(sm.xs, tid);
             __syncthreads();
         }
-        if (MODE == MODE_STEP && it == 0 && tid < PTS)
-            sm.tau[tid] += (base + tid < A.P) ? A.dtau[base + tid] : 0.0;
     }
 
     if (MODE == MODE_DIRS) {

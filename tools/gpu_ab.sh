@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 --tracking "" --no-evaluation > gpurun_out/ab_bench.json 2> gpurun_out/ab_bench.err
+python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
