@@ -172,6 +172,21 @@ __constant__ double KC[16] = {
 #endif
 
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
+// Row maxima of non-negative values through their bit patterns: for x >= 0 the IEEE order is the
+// unsigned order of the patterns, and every pattern >= DBITS_INF is inf or NaN (of either sign).
+// 4 integer instructions per 64-bit max instead of fmax's ~8 (NaN handling).
+constexpr unsigned long long DBITS_INF = 0x7ff0000000000000ull;
+__device__ __forceinline__ unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
+// 1/d for a normal d: MUFU.RCP64H seed (~20 bits) + two Newton steps (<= 1 ulp, no slow path).
+__device__ __forceinline__ double rcp_nr(double d)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -624,13 +639,24 @@ __device__ __forceinline__ void stage1(Smem<N> &sm, int tid)
 template <int N>
 __device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&row)[N + 2])
 {
-    double rmax = 0.0;
+    // the exponent of max_j |row_j|_1 is in the high words: one integer max per entry
+    unsigned hmax = 0u;
 #pragma unroll
-    for (int j = 0; j < N; ++j) rmax = fmax(rmax, cabs1(row[j]));
-    if (rmax > 0.0 && isfinite(rmax)) {
-        const double f = scalbn(1.0, -ilogb(rmax));
+    for (int j = 0; j < N; ++j) hmax = max(hmax, (unsigned)__double2hiint(cabs1(row[j])));
+    const int ef = (int)(hmax >> 20); // biased exponent (>= 0x7ff: inf/NaN)
+    if (ef >= 1 && ef <= 2045) {
+        const double f = __hiloint2double((2046 - ef) << 20, 0); // 2^-ilogb(rmax), exact
 #pragma unroll
         for (int c = 0; c < N + 2; ++c) row[c] = make_double2(row[c].x * f, row[c].y * f);
+    } else if (ef == 0 || ef == 2046) { // subnormal or [2^1023, inf) maximum (rare): general path
+        double rmax = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) rmax = fmax(rmax, cabs1(row[j]));
+        if (rmax > 0.0 && isfinite(rmax)) {
+            const double f = scalbn(1.0, -ilogb(rmax));
+#pragma unroll
+            for (int c = 0; c < N + 2; ++c) row[c] = make_double2(row[c].x * f, row[c].y * f);
+        }
     }
     double2 *dst = sm.mat + q * Geo<N>::MS + k * Geo<N>::RW;
 #pragma unroll
@@ -660,17 +686,21 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
     double2 a[RW];
 #pragma unroll
     for (int c = 0; c < RW; ++c) a[c] = slot[i * RW + c];
-    double rmax = 0.0;
+    unsigned long long rbits = 0ull;
 #pragma unroll
-    for (int j = 0; j < N; ++j) rmax = fmax(rmax, cabs1(a[j]));
+    for (int j = 0; j < N; ++j) rbits = max(rbits, dbits(cabs1(a[j])));
+    // singular threshold of this row (ledger R13); a non-finite entry makes the point singular
+    const double thr = 1e-14 * __longlong_as_double((long long)rbits);
     __syncwarp();
     bool used = false;
     col = 0;
-    singular = !isfinite(rmax);
+    singular = rbits >= DBITS_INF;
     double2 myrcp = make_double2(0.0, 0.0);
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-        const double crd = __drcp_rn(fma(a[j].x, a[j].x, a[j].y * a[j].y));
+        // 1/|a_j|^2 on every lane (its latency overlaps the pivot search).  For an accepted pivot,
+        // thr < |a_j|_1 < 2^510 keeps |a_j|^2 normal, so the Newton reciprocal is exact to 1 ulp.
+        const double crd = rcp_nr(fma(a[j].x, a[j].x, a[j].y * a[j].y));
         const double2 crcp = make_double2(a[j].x * crd, -a[j].y * crd);
         unsigned key = 0u;
         if (!used) key = ((unsigned)__double2hiint(cabs1(a[j])) & ~63u) | (unsigned)(32 - i);
@@ -710,10 +740,11 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
         }
         __syncwarp();
         const double2 rcp = slot[r * RW + j];
-        if (me) {
-            myrcp = crcp;
+        {
+            // branch-free: pivot at or below the threshold, or too large for a normal |a_j|^2
             const double pa = cabs1(a[j]);
-            if (!(pa > 1e-14 * rmax) || !isfinite(pa) || !isfinite(crd)) singular = true;
+            singular = singular || (me && !(pa > thr && pa < 0x1p510));
+            myrcp = me ? crcp : myrcp;
         }
         // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row
         double2 l = cmul(a[j], rcp);
