@@ -302,7 +302,10 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
                         if (c < N) v = cmul(v, sm.inv[q][c]);
                         else if (c == N) v = make_double2(v.x * sm.tinv[q], v.y * sm.tinv[q]);
                     }
-                    if (!scaled && e != 0) v = make_double2(scalbn(v.x, e), scalbn(v.y, e));
+                    if (!scaled && e != 0) {
+                        if (e >= -1022 && e <= 1023) v = make_double2(v.x * pow2i(e), v.y * pow2i(e));
+                        else v = make_double2(scalbn(v.x, e), scalbn(v.y, e));
+                    }
                     fin = fin && isfinite(v.x) && isfinite(v.y);
                     if (gq < A.P) {
                         if (c < N) { if (A.J) A.J[(gq * N + k) * N + c] = v; }

@@ -1,6 +1,7 @@
 // pht_kernels.cuh — sm_100a kernels for the polyhedral-homotopy hot path (arXiv 2111.14317).
 //
-// One templated kernel, k_pht<N, MODE>, covers the four entry points of include/pht.h.
+// Two templated kernels cover the entry points of include/pht.h: k_phte<N, MODE> (evaluation,
+// persistent) and k_pht<N, MODE> (directions / Euler-Newton step, evaluation + solve).
 // Mapping: a CTA owns a tile of Geo<N>::PTS points and runs two layouts.
 //  * "W" (evaluation): thread (k, q) = (equation k, point q) computes ROW k of the extended
 //    Jacobian of point q, [ dh_k/dz_1 .. dh_k/dz_N | dh_k/dtau | h_k ] (P:525-542,
@@ -177,6 +178,23 @@ __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y
 // 4 integer instructions per 64-bit max instead of fmax's ~8 (NaN handling).
 constexpr unsigned long long DBITS_INF = 0x7ff0000000000000ull;
 __device__ __forceinline__ unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
+// 2^e for a normal power of two (-1022 <= e <= 1023) from its exponent bits; 0 outside (callers
+// take scalbn there).  Multiplying by it rounds once, like scalbn.
+__device__ __forceinline__ double pow2i(int e) { return __hiloint2double((e + 1023) << 20, 0); }
+// v * 2^e (the unscaled outputs of a row with binary row exponent e): one DMUL per part
+template <int C>
+__device__ __forceinline__ void scale_row2(double2 (&row)[C], int e)
+{
+    if (e == 0) return;
+    if (e >= -1022 && e <= 1023) {
+        const double f = pow2i(e);
+#pragma unroll
+        for (int c = 0; c < C; ++c) row[c] = make_double2(row[c].x * f, row[c].y * f);
+    } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) row[c] = make_double2(scalbn(row[c].x, e), scalbn(row[c].y, e));
+    }
+}
 // 1/d for a normal d: MUFU.RCP64H seed (~20 bits) + two Newton steps (<= 1 ulp, no slow path).
 __device__ __forceinline__ double rcp_nr(double d)
 {
@@ -887,9 +905,114 @@ __device__ __forceinline__ void qsolve(Smem<N> &sm, int lane, int g, int &col, d
     dN = d2;
 }
 
+// Evaluation modes (pht_evaluate, pht_evaluate_log): one tile of the persistent kernel k_phte.
+template <int N, int MODE>
+__device__ __forceinline__ void eval_tile(const DevSys &S, const Args &A, Smem<N> &sm, const int64_t base)
+{
+    using G = Geo<N>;
+    constexpr int PTS = G::PTS, WL = G::WL;
+    const int tid = threadIdx.x;
+    const int k = tid / WL, q = tid % WL;           // W layout
+    const int64_t gq = base + q;
+    const bool valid = (k < N) && (q < PTS) && (gq < A.P);
+
+    // load the tile's points, coalesced: flat element tid = (point tid/N, variable tid%N)
+    const double2 *xsrc = A.xin;
+    if (tid < N * PTS) {
+        const int qq = tid / N, j = tid % N;
+        double2 v = make_double2(MODE == MODE_EVAL_Z ? 0.0 : 1.0, 0.0);
+        if (base + qq < A.P) v = xsrc[(base * N) + tid];
+        sm.xs[j][qq] = v;
+    }
+    if (tid < WL) {
+        sm.st[tid] = 0;
+        const int64_t g = base + tid;
+        const bool in = (tid < PTS) && (g < A.P);
+        double tv = (MODE == MODE_EVAL_Z) ? 0.0 : 1.0;
+        if (in) tv = A.tin[g];
+        if (MODE == MODE_EVAL_Z) {
+            sm.tau[tid] = tv;
+            if (!isfinite(tv)) { sm.st[tid] |= PT_NONFINITE; sm.tau[tid] = 0.0; }
+        } else {
+            if (!(tv > 0.0) || !isfinite(tv)) { sm.st[tid] |= PT_NONFINITE; tv = 1.0; }
+            sm.tau[tid] = log(tv);
+            sm.tinv[tid] = 1.0 / tv;
+        }
+        if (tid >= PTS) { // unused W lanes evaluate a harmless dummy point
+            for (int j = 0; j < N; ++j) sm.xs[j][tid] = make_double2(MODE == MODE_EVAL_Z ? 0.0 : 1.0, 0.0);
+        }
+    }
+    __syncthreads();
+    {
+        stage1<N, MODE>(sm, tid);
+        if (tid < WL && tid >= PTS)
+            for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
+        __syncthreads();
+        double2 row[N + 2];
+        int e = 0;
+        const bool wthr = k < N; // W-layout thread (the CTA is padded to whole warps)
+        if (wthr) eval_row<N>(S, sm, k, q, row, e);
+        const bool scaled = A.rexp != nullptr;
+        bool fin = true;
+        if (MODE == MODE_EVAL_X) {
+            const double ti = sm.tinv[q];
+            row[N] = make_double2(row[N].x * ti, row[N].y * ti);
+#pragma unroll
+            for (int j = 0; j < N; ++j) row[j] = cmul(row[j], sm.inv[j][q]);
+        }
+        if (!scaled) scale_row2<N + 2>(row, e);
+#pragma unroll
+        for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(row[c].x) && isfinite(row[c].y);
+        if (wthr && !fin && q < PTS) atomicOr(&sm.st[q], PT_NONFINITE);
+        if (wthr && scaled && valid) A.rexp[gq * N + k] = e;
+        // stage the tile's rows in shared memory: [q][k][0..N-1 | Jt | H], then copy each output
+        // array's contiguous block with coalesced 16-byte stores
+        if (wthr && q < PTS) {
+            double2 *dst = sm.mat + q * Geo<N>::MS + k * Geo<N>::RW;
+#pragma unroll
+            for (int c = 0; c < N + 2; ++c) dst[c] = row[c];
+        }
+        __syncthreads();
+        const int64_t npts = (A.P - base < PTS) ? (A.P - base) : PTS;
+        if (A.J) {
+            double2 *dstJ = A.J + base * N * N;
+            for (int u = tid; u < npts * N * N; u += G::NT) {
+                const int qq = u / (N * N), r = u - qq * N * N, kk = r / N, j = r - kk * N;
+                dstJ[u] = sm.mat[qq * Geo<N>::MS + kk * Geo<N>::RW + j];
+            }
+        }
+        for (int u = tid; u < npts * N; u += G::NT) {
+            const int qq = u / N, kk = u - qq * N;
+            const double2 *src = sm.mat + qq * Geo<N>::MS + kk * Geo<N>::RW;
+            if (A.Jt) A.Jt[base * N + u] = src[N];
+            if (A.H) A.H[base * N + u] = src[N + 1];
+        }
+        if (tid < PTS && base + tid < A.P && A.status) A.status[base + tid] = (uint8_t)sm.st[tid];
+    }
+}
+
+// Persistent evaluation kernel: the grid (SMs x resident CTAs, at most one CTA per tile) walks
+// the tiles and loads the exp/cis tables once per CTA (cyclic-10 evaluation 0.52 -> 0.60 G
+// points/s with the power-of-two epilogue).  The fused DIRS/STEP kernel k_pht keeps one tile per
+// CTA: a tile loop there costs live registers and spills (measured 524 -> 490 M evals/s).
+template <int N, int MODE>
+__global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_phte(const DevSys S, const Args A)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<N> &sm = *reinterpret_cast<Smem<N> *>(smem_raw);
+    load_tables(S, sm.exptab, sm.cistab, threadIdx.x, Geo<N>::NT);
+    const int64_t tiles = (A.P + Geo<N>::PTS - 1) / Geo<N>::PTS;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        eval_tile<N, MODE>(S, A, sm, t * Geo<N>::PTS);
+        __syncthreads(); // the tile's shared-memory readers are done before the next tile's loads
+    }
+}
+
+// DIRS and STEP (pht_euler_newton, pht_pc_step): evaluation + two-RHS solve, one tile per CTA.
 template <int N, int MODE>
 __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S, const Args A)
 {
+    static_assert(MODE == MODE_DIRS || MODE == MODE_STEP, "evaluation modes run k_phte");
     using G = Geo<N>;
     constexpr int PTS = G::PTS, WL = G::WL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -929,57 +1052,6 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
         }
     }
     __syncthreads();
-
-    if (MODE == MODE_EVAL_X || MODE == MODE_EVAL_Z) {
-        stage1<N, MODE>(sm, tid);
-        if (tid < WL && tid >= PTS)
-            for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
-        __syncthreads();
-        double2 row[N + 2];
-        int e = 0;
-        const bool wthr = k < N; // W-layout thread (the CTA is padded to whole warps)
-        if (wthr) eval_row<N>(S, sm, k, q, row, e);
-        const bool scaled = A.rexp != nullptr;
-        bool fin = true;
-        if (MODE == MODE_EVAL_X) {
-            const double ti = sm.tinv[q];
-            row[N] = make_double2(row[N].x * ti, row[N].y * ti);
-#pragma unroll
-            for (int j = 0; j < N; ++j) row[j] = cmul(row[j], sm.inv[j][q]);
-        }
-        if (!scaled && e != 0) {
-#pragma unroll
-            for (int c = 0; c < N + 2; ++c) row[c] = make_double2(scalbn(row[c].x, e), scalbn(row[c].y, e));
-        }
-#pragma unroll
-        for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(row[c].x) && isfinite(row[c].y);
-        if (wthr && !fin && q < PTS) atomicOr(&sm.st[q], PT_NONFINITE);
-        if (wthr && scaled && valid) A.rexp[gq * N + k] = e;
-        // stage the tile's rows in shared memory: [q][k][0..N-1 | Jt | H], then copy each output
-        // array's contiguous block with coalesced 16-byte stores
-        if (wthr && q < PTS) {
-            double2 *dst = sm.mat + q * Geo<N>::MS + k * Geo<N>::RW;
-#pragma unroll
-            for (int c = 0; c < N + 2; ++c) dst[c] = row[c];
-        }
-        __syncthreads();
-        const int64_t npts = (A.P - base < PTS) ? (A.P - base) : PTS;
-        if (A.J) {
-            double2 *dstJ = A.J + base * N * N;
-            for (int u = tid; u < npts * N * N; u += G::NT) {
-                const int qq = u / (N * N), r = u - qq * N * N, kk = r / N, j = r - kk * N;
-                dstJ[u] = sm.mat[qq * Geo<N>::MS + kk * Geo<N>::RW + j];
-            }
-        }
-        for (int u = tid; u < npts * N; u += G::NT) {
-            const int qq = u / N, kk = u - qq * N;
-            const double2 *src = sm.mat + qq * Geo<N>::MS + kk * Geo<N>::RW;
-            if (A.Jt) A.Jt[base * N + u] = src[N];
-            if (A.H) A.H[base * N + u] = src[N + 1];
-        }
-        if (tid < PTS && base + tid < A.P && A.status) A.status[base + tid] = (uint8_t)sm.st[tid];
-        return;
-    }
 
     // DIRS and STEP: evaluation (W) -> shared-memory tile -> warp-level solve (L).
     const int iters = (MODE == MODE_STEP) ? A.K + 1 : 1;
@@ -1169,10 +1241,7 @@ __global__ void __launch_bounds__(PHT_EVALP_T, 4) k_evalp(const DevSys S, const 
 #pragma unroll
             for (int j = 0; j < N; ++j) row[j] = cmul(row[j], sm.inv[j][tid]);
         }
-        if (!scaled && e != 0) {
-#pragma unroll
-            for (int c = 0; c < N + 2; ++c) row[c] = make_double2(scalbn(row[c].x, e), scalbn(row[c].y, e));
-        }
+        if (!scaled) scale_row2<N + 2>(row, e);
         bool fin = true;
 #pragma unroll
         for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(row[c].x) && isfinite(row[c].y);
@@ -1584,13 +1653,44 @@ cudaError_t launch_mode(const DevSys &S, const Args &A, cudaStream_t stream)
     return cudaGetLastError();
 }
 
+// Grid of a persistent kernel: SMs x resident CTAs per SM.
+inline int64_t persistent_grid(const void *kernel, int threads, size_t smem)
+{
+    int dev = 0, sms = 1, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    return (int64_t)(sms > 0 ? sms : 1) * (per_sm > 0 ? per_sm : 1);
+}
+
+template <int N, int MODE>
+cudaError_t launch_eval_mode(const DevSys &S, const Args &A, cudaStream_t stream)
+{
+    constexpr int PTS = Geo<N>::PTS;
+    const int64_t tiles = (A.P + PTS - 1) / PTS;
+    if (tiles == 0) return cudaSuccess;
+    const size_t sb = smem_bytes<N, MODE>();
+    static std::atomic<int64_t> full_grid[64]; // per device: SMs x resident CTAs (0: not yet configured)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int64_t fg = full_grid[dev & 63].load();
+    if (fg == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_phte<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        if (e != cudaSuccess) return e;
+        fg = persistent_grid(reinterpret_cast<const void *>(k_phte<N, MODE>), Geo<N>::NT, sb);
+        full_grid[dev & 63].store(fg);
+    }
+    k_phte<N, MODE><<<dim3((unsigned)(tiles < fg ? tiles : fg)), dim3(Geo<N>::NT), sb, stream>>>(S, A);
+    return cudaGetLastError();
+}
+
 // Host-side launcher for one n (instantiated per n in inst_n*.cu).
 template <int N>
 cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream)
 {
     switch (mode) {
-    case MODE_EVAL_X: return launch_mode<N, MODE_EVAL_X>(S, A, stream);
-    case MODE_EVAL_Z: return launch_mode<N, MODE_EVAL_Z>(S, A, stream);
+    case MODE_EVAL_X: return launch_eval_mode<N, MODE_EVAL_X>(S, A, stream);
+    case MODE_EVAL_Z: return launch_eval_mode<N, MODE_EVAL_Z>(S, A, stream);
     case MODE_DIRS: return launch_mode<N, MODE_DIRS>(S, A, stream);
     case MODE_STEP: return launch_mode<N, MODE_STEP>(S, A, stream);
     default: return cudaErrorInvalidValue;
