@@ -204,6 +204,8 @@ def hbm_peak_gbs():
 
 
 EVAL_CONFIGS = [("cyclic-10", 1 << 21, "BASELINE.json configs[2]: cyclic-10 batched H, dH/dx, dH/dt"),
+                ("cyclic-10 specialised", 1 << 21, "BASELINE.json configs[2]: cyclic-10 batched H, dH/dx, dH/dt "
+                                                   "(system-specialised kernels, pht_system_specialize)"),
                 ("random-20x50", 1 << 18, "BASELINE.json configs[3]: random dense Laurent n=20, 50 terms/eq "
                                           "(FP64 tensor-core DMMA evaluation)")]
 
@@ -219,8 +221,13 @@ def evaluation_section(world, rank, dev, reps=5):
     out = {}
     peak_bw, bw_src = hbm_peak_gbs()
     for name, Pn, label in EVAL_CONFIGS:
-        sysm = W.cyclic(10, lift_max=LIFT_MAX) if name == "cyclic-10" else W.random_dense(20, 50)
+        sysm = W.cyclic(10, lift_max=LIFT_MAX) if name.startswith("cyclic-10") else W.random_dense(20, 50)
         g = P.System.from_workload(sysm, device=dev.index)
+        spec_s = None
+        if name.endswith("specialised"):
+            t0 = time.perf_counter()
+            g.specialize()  # NVRTC compile of the generated rows: outside the timed region
+            spec_s = time.perf_counter() - t0
         x, t, _ = W.random_points(Pn, sysm.n, seed=2000 + rank, rho_max=0.5 if sysm.n > 12 else 1.0)
         xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
         n = sysm.n
@@ -252,7 +259,10 @@ def evaluation_section(world, rank, dev, reps=5):
                      "fp64": {"achieved_tflops": fl / (ms * 1e-3) / 1e12, "peak_tflops": fp64_peak_tflops(1965.0),
                               "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak_tflops(1965.0),
                               "flops_per_point": fl / Pn},
-                     "path": "FP64 tensor cores (DMMA)" if g.dense else "scalar FP64 kernel"}
+                     "path": ("system-specialised point-per-thread kernel (NVRTC)" if spec_s is not None else
+                              "FP64 tensor cores (DMMA)" if g.dense else "scalar FP64 kernel")}
+        if spec_s is not None:
+            out[name]["specialize_s"] = spec_s
         del g, xd, td, H, J, Jt, st
     return out
 
