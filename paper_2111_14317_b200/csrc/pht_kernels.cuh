@@ -1022,8 +1022,6 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
     const int lane = tid & 31, warp = tid >> 5;      // L layout
     load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
     const int64_t base = (int64_t)blockIdx.x * PTS;
-    const int64_t gq = base + q;
-    const bool valid = (k < N) && (q < PTS) && (gq < A.P);
 
     // load the tile's points, coalesced: flat element tid = (point tid/N, variable tid%N)
     const double2 *xsrc = (MODE == MODE_STEP) ? A.xio : A.xin;
