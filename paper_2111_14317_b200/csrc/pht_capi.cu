@@ -441,7 +441,7 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     if (A0.P == 0) return PHT_OK;
     DevGuard g(s->device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
-    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj};
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj, s->max_terms};
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     pht::Args A = A0;
@@ -706,7 +706,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     cudaError_t e;
     if ((e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
-    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj};
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj, s->max_terms};
     pht::TrackArgs A{};
     A.P = p;
     A.x = (double2 *)x;

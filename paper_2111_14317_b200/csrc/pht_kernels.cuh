@@ -57,6 +57,7 @@ struct DevSys {
     const double2 *cistab; // [256] (cos, sin)(2 pi j / 256)
     int n;
     int proj; // projective system: N = n_eq + 1 homogeneous coordinates, row N-1 = y^*
+    int mt;   // most terms of one equation (k_stepw's shared-memory record table)
 };
 
 struct Args {
@@ -655,7 +656,7 @@ __device__ __forceinline__ void stage1(Smem<N> &sm, int tid)
 // W -> shared: normalise the row by an exact power of two (rows are scale-free for the solve,
 // S:316) and store it into the point's matrix slot.
 template <int N>
-__device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&row)[N + 2])
+__device__ __forceinline__ void normalize_row(double2 (&row)[N + 2])
 {
     // the exponent of max_j |row_j|_1 is in the high words: one integer max per entry
     unsigned hmax = 0u;
@@ -676,6 +677,12 @@ __device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&r
             for (int c = 0; c < N + 2; ++c) row[c] = make_double2(row[c].x * f, row[c].y * f);
         }
     }
+}
+
+template <int N>
+__device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&row)[N + 2])
+{
+    normalize_row<N>(row);
     double2 *dst = sm.mat + q * Geo<N>::MS + k * Geo<N>::RW;
 #pragma unroll
     for (int c = 0; c < N + 2; ++c) dst[c] = row[c];
@@ -688,22 +695,13 @@ __device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&r
 // row; elimination is branch-free (multiplier 0 on the pivot lane).  On return the lane whose row
 // pivoted column `col` holds dE = -row[N]/u, dN = -row[N+1]/u for variable col:
 // G [dE | dN] = -[G_tau | h].
-template <int N>
-__device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int &col, double2 &dE,
-                                       double2 &dN, bool &singular, bool &act, int &q)
+// The elimination on rows held in registers: lane (seg0 = lane / N, i) holds row i of its point;
+// prow: the point's pivot-row buffer (N + 2 entries, shared memory), kseg: its pivot keys (PPW > 4).
+template <int N, int PPW, int KS>
+__device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, unsigned *kseg, int seg0, int seg,
+                                            int i, bool act, int &col, double2 &dE, double2 &dN, bool &singular)
 {
-    constexpr int RW = Geo<N>::RW, MS = Geo<N>::MS, PPW = Geo<N>::PPW, KS = Geo<N>::KS;
-    const int seg0 = lane / N;
-    const bool inseg = seg0 < PPW;
-    const int seg = inseg ? seg0 : 0, i = inseg ? lane - seg0 * N : 0;
-    q = g * PPW + seg;
-    act = inseg && (q < Geo<N>::PTS);
-    const int qc = (q < Geo<N>::PTS) ? q : 0;
-    double2 *slot = sm.mat + qc * MS;
-    unsigned *kseg = &sm.keys[w][seg * KS];
-    double2 a[RW];
-#pragma unroll
-    for (int c = 0; c < RW; ++c) a[c] = slot[i * RW + c];
+    constexpr int RW = N + 2;
     unsigned long long rbits = 0ull;
 #pragma unroll
     for (int j = 0; j < N; ++j) rbits = max(rbits, dbits(cabs1(a[j])));
@@ -752,12 +750,12 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
             // the pivot row with the pivot replaced by its reciprocal (computed before the
             // argmax by every lane for its own candidate: the reciprocal's latency overlaps the
             // pivot search instead of following the row broadcast)
-            slot[r * RW + j] = crcp;
+            prow[j] = crcp;
 #pragma unroll
-            for (int c = j + 1; c < RW; ++c) slot[r * RW + c] = a[c];
+            for (int c = j + 1; c < RW; ++c) prow[c] = a[c];
         }
         __syncwarp();
-        const double2 rcp = slot[r * RW + j];
+        const double2 rcp = prow[j];
         {
             // branch-free: pivot at or below the threshold, or too large for a normal |a_j|^2
             const double pa = cabs1(a[j]);
@@ -768,13 +766,34 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
         double2 l = cmul(a[j], rcp);
         l = me ? make_double2(0.0, 0.0) : l;
 #pragma unroll
-        for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, slot[r * RW + c]);
+        for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, prow[c]);
         a[j] = me ? a[j] : make_double2(0.0, 0.0);
         __syncwarp();
     }
     const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
     dE = make_double2(-e.x, -e.y);
     dN = make_double2(-n.x, -n.y);
+}
+
+// a5 in the L layout of the tile kernels: the rows come from the point's matrix slot
+template <int N>
+__device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int &col, double2 &dE,
+                                       double2 &dN, bool &singular, bool &act, int &q)
+{
+    constexpr int RW = Geo<N>::RW, MS = Geo<N>::MS, PPW = Geo<N>::PPW, KS = Geo<N>::KS;
+    const int seg0 = lane / N;
+    const bool inseg = seg0 < PPW;
+    const int seg = inseg ? seg0 : 0, i = inseg ? lane - seg0 * N : 0;
+    q = g * PPW + seg;
+    act = inseg && (q < Geo<N>::PTS);
+    const int qc = (q < Geo<N>::PTS) ? q : 0;
+    double2 *slot = sm.mat + qc * MS;
+    unsigned *kseg = &sm.keys[w][seg * KS];
+    double2 a[RW];
+#pragma unroll
+    for (int c = 0; c < RW; ++c) a[c] = slot[i * RW + c];
+    __syncwarp(); // every row is in registers before the slot doubles as the pivot-row buffer
+    lsolve_regs<N, PPW, KS>(a, slot, kseg, seg0, seg, i, act, col, dE, dN, singular);
 }
 
 // y <- y / ||y|| for the point q of a [variable][point] tile (projective systems, reading R29)
@@ -1162,6 +1181,209 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
     }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Warp-per-group Euler-Newton step (pht_pc_step, LU, affine).  One warp owns a
+// group of PPW = 32/N points and keeps ONE lane mapping through every stage: lane (q, i) = (point
+// q of the group, index i).  It loads x_i, runs stage 1 for variable i, evaluates ROW i of the
+// point's extended Jacobian (stage 2-4, equation i) into registers, and that row is the row the
+// lane holds in the Gauss-Jordan solve -- no shared-memory matrix tile, no staging of rows, no
+// CTA barriers (warps of a CTA only share the exp/cis tables and the term records, loaded once:
+// the kernel is persistent).  The records sit in shared memory term-major, R[t][k], so the lanes
+// of one step of the term loop read neighbouring records.
+template <int N>
+struct GeoW {
+    static constexpr int PPW = 32 / N; // points per warp
+#ifndef PHT_STEPW_WARPS
+#define PHT_STEPW_WARPS 8
+#endif
+#ifndef PHT_STEPW_MINB
+#define PHT_STEPW_MINB 2
+#endif
+    static constexpr int WARPS = PHT_STEPW_WARPS;
+    static constexpr int NT = WARPS * 32;
+    static constexpr int RW = N + 2;
+    static constexpr int KS = (N + 3) & ~3;
+    static constexpr int MINB = PHT_STEPW_MINB; // 16 warps per SM at <= 128 registers (4 x 4: -1%, 4 x 5: spills)
+};
+
+template <int N>
+struct SmemW {
+    double exptab[TAB_E];
+    double2 cistab[TAB_C];
+    struct Warp {
+        double2 rt[N][GeoW<N>::PPW];                // (rho, vartheta) of the group's points
+        double2 xs[N][GeoW<N>::PPW];                // x of the group's points
+        double2 prow[GeoW<N>::PPW][GeoW<N>::RW | 1]; // pivot-row buffer per point (odd stride)
+        alignas(16) unsigned keys[GeoW<N>::PPW * GeoW<N>::KS];
+        double dn2[N][GeoW<N>::PPW];
+        double tau[GeoW<N>::PPW];
+        int st[GeoW<N>::PPW];
+    } w[GeoW<N>::WARPS];
+    int mk[N]; // terms per equation
+    // followed by the records R[MT][N][rec_stride(N) / 2] (double2)
+};
+
+template <int N>
+__device__ __forceinline__ void load_rec_s(const double2 *r, double (&a)[rec_stride(N)])
+{
+#pragma unroll
+    for (int u = 0; u < rec_stride(N) / 2; ++u) {
+        const double2 v = r[u];
+        a[2 * u] = v.x;
+        a[2 * u + 1] = v.y;
+    }
+}
+
+// stages 2-4 for row k of group point q (records from shared memory, term-major)
+template <int N>
+__device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R, const typename SmemW<N>::Warp &W,
+                                           int k, int q, double2 (&row)[N + 2], int &e)
+{
+    constexpr int RS = rec_stride(N), PPW = GeoW<N>::PPW;
+    PointLog<N, true> pl;
+    pl.base = &W.rt[0][q];
+    pl.stride = PPW;
+    const double tau = W.tau[q];
+    const int m = sm.mk[k];
+    const double2 *rec = R + (size_t)k * (RS / 2);
+    constexpr size_t TS = (size_t)N * (RS / 2); // record stride between terms of one equation
+    RowAcc<N> acc;
+    {
+        double a[RS];
+        load_rec_s<N>(rec, a);
+        acc.init(phi_of<N>(a, pl, tau));
+    }
+    int i = 0;
+    for (; PHT_PAIR(N) && i + 1 < m; i += 2) {
+        double a[RS], b[RS];
+        load_rec_s<N>(rec + (size_t)i * TS, a);
+        load_rec_s<N>(rec + (size_t)(i + 1) * TS, b);
+        double pa, pb, ta, tb;
+        phi_theta<N>(a, pl, tau, pa, ta);
+        phi_theta<N>(b, pl, tau, pb, tb);
+        acc.reduce(pa);
+        acc.reduce(pb);
+        const double ya = acc.reduced(pa), yb = acc.reduced(pb);
+        const double2 wa = expcis(ya, ta, sm.exptab, sm.cistab);
+        const double2 wb = expcis(yb, tb, sm.exptab, sm.cistab);
+        acc.add(a, wa);
+        acc.add(b, wb);
+    }
+    for (; i < m; ++i) {
+        double a[RS];
+        load_rec_s<N>(rec + (size_t)i * TS, a);
+        double pa, ta;
+        phi_theta<N>(a, pl, tau, pa, ta);
+        const double ya = acc.reduce(pa);
+        acc.add(a, expcis(ya, ta, sm.exptab, sm.cistab));
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) row[j] = acc.g[j];
+    row[N] = acc.gt;
+    row[N + 1] = acc.h;
+    e = (int)acc.ed;
+}
+
+template <int N>
+__global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_stepw(const DevSys S, const Args A, int MT)
+{
+    using G = GeoW<N>;
+    constexpr int RS = rec_stride(N), PPW = G::PPW;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmemW<N> &sm = *reinterpret_cast<SmemW<N> *>(smem_raw);
+    double2 *R = reinterpret_cast<double2 *>(smem_raw + ((sizeof(SmemW<N>) + 15) & ~(size_t)15));
+    const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
+    for (int idx = tid; idx < MT * N * (RS / 2); idx += G::NT) { // records, term-major
+        const int u = idx % (RS / 2), kk = (idx / (RS / 2)) % N, t = idx / ((RS / 2) * N);
+        const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
+        R[idx] = (t < m) ? __ldg(S.rec + (size_t)(i0 + t) * (RS / 2) + u) : make_double2(0.0, 0.0);
+    }
+    if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
+    __syncthreads();
+    typename SmemW<N>::Warp &W = sm.w[wi];
+    // lane = i * PPW + q (index-major): the PPW lanes of one index read the same term record
+    // (a broadcast), so a record load touches N distinct 16-byte chunks, not N per point
+    const bool inseg = lane < N * PPW;
+    const int q = inseg ? lane % PPW : 0, i = inseg ? lane / PPW : 0; // point of the group, index
+    const int seg0 = inseg ? q : PPW;                                 // segment (PPW: no point)
+    const int64_t groups = (A.P + PPW - 1) / PPW;
+    for (int64_t grp = (int64_t)blockIdx.x * G::WARPS + wi; grp < groups; grp += (int64_t)gridDim.x * G::WARPS) {
+        const int64_t base = grp * PPW, gp = base + q;
+        const bool act = inseg && gp < A.P;
+        double2 xv = make_double2(1.0, 0.0); // lanes of points past P carry a harmless dummy
+        if (act) xv = A.xio[gp * N + i];
+        if (lane < PPW) {
+            double tv = (base + lane < A.P) ? A.tauio[base + lane] : 0.0;
+            int st = 0;
+            if (!isfinite(tv)) { st = PT_NONFINITE; tv = 0.0; }
+            W.tau[lane] = tv;
+            W.st[lane] = st;
+        }
+        __syncwarp();
+        {
+            double rho, th;
+            double2 iv;
+            int st = 0;
+            log_split(xv, rho, th, iv, st); // a1 for variable i
+            if (inseg) {
+                W.rt[i][q] = make_double2(rho, th);
+                W.xs[i][q] = xv;
+                W.dn2[i][q] = 0.0;
+            }
+            if (st && act) atomicOr(&W.st[q], st);
+        }
+        __syncwarp();
+        for (int it = 0; it <= A.K; ++it) {
+            double2 a[N + 2];
+            int e;
+            eval_row_w<N>(sm, R, W, i, q, a, e); // row i of point q: [dh_i/dz | dh_i/dtau | h_i] 2^-e
+            normalize_row<N>(a);
+            __syncwarp(); // every lane has read tau and (rho, vartheta)
+            if (it == 0 && lane < PPW && base + lane < A.P) W.tau[lane] += A.dtau[base + lane];
+            int col;
+            double2 dE, dN;
+            bool sing;
+            lsolve_regs<N, PPW, G::KS>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, act, col, dE, dN, sing);
+            if (act) { // the lane whose row pivoted column col updates variable col
+                if (sing) atomicOr(&W.st[q], PT_SINGULAR);
+                const double2 xo = W.xs[col][q];
+                double2 xn;
+                if (it == 0) { // Euler: x~ = x + h x (.) delta_E
+                    const double h = A.dtau[gp];
+                    const double2 d = cmul(xo, dE);
+                    xn = make_double2(fma(h, d.x, xo.x), fma(h, d.y, xo.y));
+                } else {       // Newton: x~ = x~ + x~ (.) delta_N
+                    const double2 d = cmul(xo, dN);
+                    xn = make_double2(xo.x + d.x, xo.y + d.y);
+                    W.dn2[col][q] = fma(d.x, d.x, d.y * d.y);
+                }
+                W.xs[col][q] = xn;
+                if (it < A.K) { // stage 1 of the next evaluation, for this coordinate
+                    double rho, th;
+                    double2 iv;
+                    int st = 0;
+                    log_split(xn, rho, th, iv, st);
+                    W.rt[col][q] = make_double2(rho, th);
+                    if (st) atomicOr(&W.st[q], st);
+                }
+            }
+            __syncwarp();
+        }
+        if (act) A.xio[gp * N + i] = W.xs[i][q];
+        if (lane < PPW && base + lane < A.P) {
+            A.tauio[base + lane] = W.tau[lane];
+            if (A.status) A.status[base + lane] = (uint8_t)W.st[lane];
+            if (A.dnnorm) {
+                double s2 = 0.0;
+                for (int j = 0; j < N; ++j) s2 += W.dn2[j][lane];
+                A.dnnorm[base + lane] = A.K > 0 ? sqrt(s2) : 0.0;
+            }
+        }
+        __syncwarp();
+    }
+}
 
 #ifdef PHT_JIT
 // ---------------------------------------------------------------------------------------
@@ -1682,6 +1904,45 @@ cudaError_t launch_eval_mode(const DevSys &S, const Args &A, cudaStream_t stream
     return cudaGetLastError();
 }
 
+// k_stepw: affine systems, LU solver, n <= 12 (the tile kernel keeps (rho, vartheta) in registers
+// from n = 13 on and is faster there: cyclic-14 174 vs 154 M evals/s), records in shared memory
+// (max_terms = MT per equation); PHT_STEPW=0 selects the tile kernel k_pht (experiments).
+template <int N>
+bool stepw_eligible(const DevSys &S, const Args &A)
+{
+    if (N > 12 || S.proj || A.solver != SOLVER_LU || S.mt <= 0) return false;
+    const char *ev = getenv("PHT_STEPW");
+    return !(ev && ev[0] == '0');
+}
+
+template <int N>
+cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
+{
+    constexpr int PPW = GeoW<N>::PPW;
+    const int64_t groups = (A.P + PPW - 1) / PPW;
+    if (groups == 0) return cudaSuccess;
+    const size_t sb = ((sizeof(SmemW<N>) + 15) & ~(size_t)15) + (size_t)S.mt * N * rec_stride(N) * sizeof(double);
+    if (sb > 200 * 1024) return cudaErrorNotSupported;
+    // per device: the largest shared-memory size configured so far and the grid for the last size
+    static std::atomic<int64_t> conf_sb[64], last_sb[64], last_fg[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if ((int64_t)sb > conf_sb[dev & 63].load()) {
+        cudaError_t e = cudaFuncSetAttribute(k_stepw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        if (e != cudaSuccess) return e;
+        conf_sb[dev & 63].store((int64_t)sb);
+    }
+    int64_t fg = (last_sb[dev & 63].load() == (int64_t)sb) ? last_fg[dev & 63].load() : 0;
+    if (fg == 0) {
+        fg = persistent_grid(reinterpret_cast<const void *>(k_stepw<N>), GeoW<N>::NT, sb);
+        last_fg[dev & 63].store(fg);
+        last_sb[dev & 63].store((int64_t)sb);
+    }
+    const int64_t need = (groups + GeoW<N>::WARPS - 1) / GeoW<N>::WARPS;
+    k_stepw<N><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
+    return cudaGetLastError();
+}
+
 // Host-side launcher for one n (instantiated per n in inst_n*.cu).
 template <int N>
 cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream)
@@ -1690,7 +1951,11 @@ cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream
     case MODE_EVAL_X: return launch_eval_mode<N, MODE_EVAL_X>(S, A, stream);
     case MODE_EVAL_Z: return launch_eval_mode<N, MODE_EVAL_Z>(S, A, stream);
     case MODE_DIRS: return launch_mode<N, MODE_DIRS>(S, A, stream);
-    case MODE_STEP: return launch_mode<N, MODE_STEP>(S, A, stream);
+    case MODE_STEP: {
+        cudaError_t e = cudaErrorNotSupported;
+        if (stepw_eligible<N>(S, A)) e = launch_stepw<N>(S, A, stream);
+        return e == cudaErrorNotSupported ? launch_mode<N, MODE_STEP>(S, A, stream) : e;
+    }
     default: return cudaErrorInvalidValue;
     }
 }
