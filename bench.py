@@ -568,7 +568,7 @@ def main():
                        "l2": "inputs larger than L2 (state %.0f MB > 126 MB)" % (Pn * (16 * N_VARS + 24) / 1e6)},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": step_traffic(Pn),
-                         "kernel": "k_pht<10, MODE_STEP>",
+                         "kernel": "k_stepw<10> (warp-per-group Euler-Newton step)",
                          "peak_basis": f"FP64 148 SM x 64 FMA/clk x 2 x {peak_mhz:.0f} MHz (DESIGN.md §5)",
                          "flops_per_point_step": 2 * fl["total"]},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pn * (16 * N_VARS + 16),

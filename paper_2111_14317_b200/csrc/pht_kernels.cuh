@@ -1510,8 +1510,8 @@ struct TrackSmem {
     int active;
 };
 
-template <int N>
-__device__ __forceinline__ void trk_pop(TrackSmem<N> &T, const TrackArgs &A, int q)
+template <int N, class TT>
+__device__ __forceinline__ void trk_pop(TT &T, const TrackArgs &A, int q)
 {
     unsigned long long idx = atomicAdd(A.queue, 1ull);
     while ((long long)idx < A.P && !isfinite(A.tau[idx])) { // unusable start: report and skip
@@ -1546,8 +1546,8 @@ __device__ __forceinline__ void trk_pop(TrackSmem<N> &T, const TrackArgs &A, int
     }
 }
 
-template <int N>
-__device__ __forceinline__ void trk_finish(TrackSmem<N> &T, const TrackArgs &A, int q, int status)
+template <int N, class TT>
+__device__ __forceinline__ void trk_finish(TT &T, const TrackArgs &A, int q, int status)
 {
     const long long pth = T.path[q];
     A.status[pth] = (uint8_t)status;
@@ -1586,6 +1586,90 @@ __device__ __forceinline__ double2 trk_update(double2 v, double2 delta, double h
     if (LOGS) return zlog1p_add(v, make_double2(h * delta.x, h * delta.y));
     const double2 d = cmul(v, delta);
     return make_double2(fma(h, d.x, v.x), fma(h, d.y, v.y));
+}
+
+// (4) of the tracker: the per-slot decisions of one iteration (the oracle's control flow, oracle.c
+// orc_track); T: the tile tracker's TrackSmem or the warp tracker's per-warp state (same fields).
+template <int N, bool LOGS, class TT>
+__device__ __forceinline__ void trk_decide(TT &T, const TrackArgs &A, const DevSys &S, int qq, int bad)
+{
+    const TrackOpts &o = A.o;
+    const int ph = T.phase[qq];
+    T.evals[qq] += 1;
+    int finish = -1; // status when the path ends this iteration
+    bool reject = false;
+    if (ph == PH_PREDICT) {
+        if (bad) reject = true;
+        else {
+            T.tau_t[qq] = T.tau_a[qq] + fmin(T.dt[qq], -T.tau_a[qq]);
+            T.phase[qq] = PH_CORRECT;
+            T.it[qq] = 1;
+            T.prev[qq] = INFINITY;
+        }
+    } else if (ph == PH_CORRECT) {
+        if (bad) reject = true;
+        else {
+            double nd = 0.0; // max_j |dx_j| / |x_j| (componentwise relative, reading R14)
+            for (int j = 0; j < N; ++j) nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
+            nd = sqrt(nd);      // projective: ||dy|| (||y|| = 1, reading R29)
+            if (T.it[qq] == 1) T.nd1[qq] = nd;
+            // converged: the update, or the update times the observed contraction (the
+            // quadratic-convergence estimate of the remaining error), <= newton_tol (R14)
+            if (nd <= o.newton_tol || (T.it[qq] >= 2 && nd * (nd / T.prev[qq]) <= o.newton_tol)) {
+                T.acc[qq] = 1;
+                T.tau_p[qq] = T.tau_a[qq];
+                T.has_prev[qq] = 1;
+                T.tau_a[qq] = T.tau_t[qq];
+                T.steps[qq] += 1;
+                if (o.pred_tol > 0.0) { // next step from the Euler predictor's error, O(dtau^2)
+                    const double e1 = T.nd1[qq];
+                    const double f = (e1 > 0.0) ? fmin(fmax(sqrt(o.pred_tol / e1), o.shrink), o.grow) : o.grow;
+                    T.dt[qq] = fmin(f * T.dt[qq], o.dtau_max);
+                } else if (++T.succ[qq] == o.grow_after) {
+                    T.dt[qq] = fmin(o.grow * T.dt[qq], o.dtau_max);
+                    T.succ[qq] = 0;
+                }
+                T.phase[qq] = (T.tau_a[qq] < 0.0) ? PH_PREDICT : PH_FINAL;
+                if (T.phase[qq] == PH_PREDICT && T.steps[qq] == o.max_steps) finish = 16; // MAX_STEPS
+            } else if ((T.it[qq] >= 2 && nd > 0.5 * T.prev[qq]) || T.it[qq] >= o.K) {
+                reject = true;
+            } else {
+                T.prev[qq] = nd;
+                T.it[qq] += 1;
+            }
+        }
+    } else { // FINAL
+        T.fin[qq] += 1;
+        if (bad) finish = 32;
+        else {
+            double nd = 0.0, xinf = 0.0; // xinf: max |x_j| (or max Re z_j in log state)
+            for (int j = 0; j < N; ++j) {
+                nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
+                const double2 v = T.xa[j][qq];
+                xinf = fmax(xinf, LOGS ? v.x : sqrt(fma(v.x, v.x, v.y * v.y)));
+            }
+            const double2 yn = T.xa[N - 1][qq]; // projective: finite iff |y_n| >= 1 / inf_norm
+            const bool finite = S.proj ? (sqrt(fma(yn.x, yn.x, yn.y * yn.y)) * o.inf_norm >= 1.0)
+                                       : (LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm));
+            if (sqrt(nd) <= o.final_tol) finish = finite ? 0 : 32;
+            else if (T.fin[qq] >= o.final_iters) // accuracy floor: accept at newton_tol (R14)
+                finish = (sqrt(nd) <= o.newton_tol && finite) ? 0 : 32;
+        }
+    }
+    if (reject) {
+        T.rej[qq] += 1;
+        T.dt[qq] *= o.shrink;
+        T.succ[qq] = 0;
+        if (T.dt[qq] < o.dtau_min) finish = (bad & PT_SINGULAR) ? PT_SINGULAR : 8; // STEP_UNDERFLOW
+        else {
+            T.phase[qq] = PH_PREDICT;
+            if (T.steps[qq] == o.max_steps) finish = 16;
+        }
+    }
+    if (finish >= 0) {
+        trk_finish<N>(T, A, qq, finish);
+        trk_pop<N>(T, A, qq);
+    }
 }
 
 template <int N, bool LOGS>
@@ -1724,85 +1808,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
         }
         // (4) per-slot decisions (the oracle's control flow, oracle.c orc_track)
         if (tid < PTS && T.phase[tid] != PH_IDLE) {
-            const int qq = tid;
-            const int ph = T.phase[qq];
-            const int bad = sm.st[qq];
-            T.evals[qq] += 1;
-            int finish = -1; // status when the path ends this iteration
-            bool reject = false;
-            if (ph == PH_PREDICT) {
-                if (bad) reject = true;
-                else {
-                    T.tau_t[qq] = T.tau_a[qq] + fmin(T.dt[qq], -T.tau_a[qq]);
-                    T.phase[qq] = PH_CORRECT;
-                    T.it[qq] = 1;
-                    T.prev[qq] = INFINITY;
-                }
-            } else if (ph == PH_CORRECT) {
-                if (bad) reject = true;
-                else {
-                    double nd = 0.0; // max_j |dx_j| / |x_j| (componentwise relative, reading R14)
-                    for (int j = 0; j < N; ++j) nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
-                    nd = sqrt(nd);      // projective: ||dy|| (||y|| = 1, reading R29)
-                    if (T.it[qq] == 1) T.nd1[qq] = nd;
-                    // converged: the update, or the update times the observed contraction (the
-                    // quadratic-convergence estimate of the remaining error), <= newton_tol (R14)
-                    if (nd <= o.newton_tol || (T.it[qq] >= 2 && nd * (nd / T.prev[qq]) <= o.newton_tol)) {
-                        T.acc[qq] = 1;
-                        T.tau_p[qq] = T.tau_a[qq];
-                        T.has_prev[qq] = 1;
-                        T.tau_a[qq] = T.tau_t[qq];
-                        T.steps[qq] += 1;
-                        if (o.pred_tol > 0.0) { // next step from the Euler predictor's error, O(dtau^2)
-                            const double e1 = T.nd1[qq];
-                            const double f = (e1 > 0.0) ? fmin(fmax(sqrt(o.pred_tol / e1), o.shrink), o.grow) : o.grow;
-                            T.dt[qq] = fmin(f * T.dt[qq], o.dtau_max);
-                        } else if (++T.succ[qq] == o.grow_after) {
-                            T.dt[qq] = fmin(o.grow * T.dt[qq], o.dtau_max);
-                            T.succ[qq] = 0;
-                        }
-                        T.phase[qq] = (T.tau_a[qq] < 0.0) ? PH_PREDICT : PH_FINAL;
-                        if (T.phase[qq] == PH_PREDICT && T.steps[qq] == o.max_steps) finish = 16; // MAX_STEPS
-                    } else if ((T.it[qq] >= 2 && nd > 0.5 * T.prev[qq]) || T.it[qq] >= o.K) {
-                        reject = true;
-                    } else {
-                        T.prev[qq] = nd;
-                        T.it[qq] += 1;
-                    }
-                }
-            } else { // FINAL
-                T.fin[qq] += 1;
-                if (bad) finish = 32;
-                else {
-                    double nd = 0.0, xinf = 0.0; // xinf: max |x_j| (or max Re z_j in log state)
-                    for (int j = 0; j < N; ++j) {
-                        nd = S.proj ? nd + T.nd2[j][qq] : fmax(nd, T.nd2[j][qq]);
-                        const double2 v = T.xa[j][qq];
-                        xinf = fmax(xinf, LOGS ? v.x : sqrt(fma(v.x, v.x, v.y * v.y)));
-                    }
-                    const double2 yn = T.xa[N - 1][qq]; // projective: finite iff |y_n| >= 1 / inf_norm
-                    const bool finite = S.proj ? (sqrt(fma(yn.x, yn.x, yn.y * yn.y)) * o.inf_norm >= 1.0)
-                                               : (LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm));
-                    if (sqrt(nd) <= o.final_tol) finish = finite ? 0 : 32;
-                    else if (T.fin[qq] >= o.final_iters) // accuracy floor: accept at newton_tol (R14)
-                        finish = (sqrt(nd) <= o.newton_tol && finite) ? 0 : 32;
-                }
-            }
-            if (reject) {
-                T.rej[qq] += 1;
-                T.dt[qq] *= o.shrink;
-                T.succ[qq] = 0;
-                if (T.dt[qq] < o.dtau_min) finish = (bad & PT_SINGULAR) ? PT_SINGULAR : 8; // STEP_UNDERFLOW
-                else {
-                    T.phase[qq] = PH_PREDICT;
-                    if (T.steps[qq] == o.max_steps) finish = 16;
-                }
-            }
-            if (finish >= 0) {
-                trk_finish<N>(T, A, qq, finish);
-                trk_pop<N>(T, A, qq);
-            }
-            if (T.phase[qq] != PH_IDLE) atomicAdd(&T.active, 1);
+            trk_decide<N, LOGS>(T, A, S, tid, sm.st[tid]);
+            if (T.phase[tid] != PH_IDLE) atomicAdd(&T.active, 1);
         }
         __syncthreads();
         if (T.active == 0) {
@@ -1816,7 +1823,245 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Warp-per-group tracker (n <= 12, LU, affine/log/cell state, Euler predictor): the k_stepw
+// lane mapping (lane = i * PPW + q) with the tracker's state machine per warp -- each warp runs
+// PPW path slots on its own (no CTA barriers); the warps of a CTA share the exp/cis tables and the
+// term records (shared memory, loaded once).  Same control flow as k_track (trk_decide).
+template <int N>
+struct TrackW {
+    static constexpr int PPW = GeoW<N>::PPW;
+    double2 rt[N][PPW];                 // (rho, vartheta) of the query points
+    double2 xa[N][PPW], xt[N][PPW];     // accepted and trial points
+    double2 dd[N][PPW];                 // direction of this iteration
+    double nd2[N][PPW];
+    double2 prow[PPW][GeoW<N>::RW | 1];
+    alignas(16) unsigned keys[PPW * GeoW<N>::KS];
+    double tau[PPW];                    // query tau
+    double tau_a[PPW], tau_t[PPW], dt[PPW], prev[PPW], nd1[PPW], tau_p[PPW];
+    long long path[PPW], steps[PPW], rej[PPW], evals[PPW], fin[PPW], done_path[PPW];
+    int phase[PPW], it[PPW], succ[PPW], cell[PPW], acc[PPW], refill[PPW], has_prev[PPW], st[PPW];
+};
+
+template <int N>
+struct SmemTW {
+    double exptab[TAB_E];
+    double2 cistab[TAB_C];
+    TrackW<N> w[GeoW<N>::WARPS];
+    int mk[N], off[N + 1];
+    // followed by the records R[MT][N][rec_stride(N) / 2]
+};
+
+// row k of group point q for the tracker: records from shared memory; cell mode replaces each
+// term's omega by the path's shifted lifting wq[global term index]
+template <int N>
+__device__ __forceinline__ void eval_row_tw(const SmemTW<N> &sm, const double2 *R, const TrackW<N> &W, int k, int q,
+                                            const double *wq, double2 (&row)[N + 2], int &e)
+{
+    constexpr int RS = rec_stride(N), PPW = GeoW<N>::PPW;
+    PointLog<N, true> pl;
+    pl.base = &W.rt[0][q];
+    pl.stride = PPW;
+    const double tau = W.tau[q];
+    const int m = sm.mk[k];
+    const double2 *rec = R + (size_t)k * (RS / 2);
+    constexpr size_t TS = (size_t)N * (RS / 2);
+    const double *wk = wq ? wq + sm.off[k] : nullptr;
+    RowAcc<N> acc;
+    {
+        double a[RS];
+        load_rec_s<N>(rec, a);
+        if (wk) a[N] = __ldg(wk);
+        acc.init(phi_of<N>(a, pl, tau));
+    }
+    int i = 0;
+    for (; PHT_PAIR(N) && i + 1 < m; i += 2) {
+        double a[RS], b[RS];
+        load_rec_s<N>(rec + (size_t)i * TS, a);
+        load_rec_s<N>(rec + (size_t)(i + 1) * TS, b);
+        if (wk) {
+            a[N] = __ldg(wk + i);
+            b[N] = __ldg(wk + i + 1);
+        }
+        double pa, pb, ta, tb;
+        phi_theta<N>(a, pl, tau, pa, ta);
+        phi_theta<N>(b, pl, tau, pb, tb);
+        acc.reduce(pa);
+        acc.reduce(pb);
+        const double ya = acc.reduced(pa), yb = acc.reduced(pb);
+        const double2 wa = expcis(ya, ta, sm.exptab, sm.cistab);
+        const double2 wb = expcis(yb, tb, sm.exptab, sm.cistab);
+        acc.add(a, wa);
+        acc.add(b, wb);
+    }
+    for (; i < m; ++i) {
+        double a[RS];
+        load_rec_s<N>(rec + (size_t)i * TS, a);
+        if (wk) a[N] = __ldg(wk + i);
+        double pa, ta;
+        phi_theta<N>(a, pl, tau, pa, ta);
+        const double ya = acc.reduce(pa);
+        acc.add(a, expcis(ya, ta, sm.exptab, sm.cistab));
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) row[j] = acc.g[j];
+    row[N] = acc.gt;
+    row[N + 1] = acc.h;
+    e = (int)acc.ed;
+}
+
+template <int N, bool LOGS>
+__global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const DevSys S, const TrackArgs A, int MT)
+{
+    using G = GeoW<N>;
+    constexpr int RS = rec_stride(N), PPW = G::PPW;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmemTW<N> &sm = *reinterpret_cast<SmemTW<N> *>(smem_raw);
+    double2 *R = reinterpret_cast<double2 *>(smem_raw + ((sizeof(SmemTW<N>) + 15) & ~(size_t)15));
+    const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    const TrackOpts &o = A.o;
+    load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
+    for (int idx = tid; idx < MT * N * (RS / 2); idx += G::NT) { // records, term-major
+        const int u = idx % (RS / 2), kk = (idx / (RS / 2)) % N, t = idx / ((RS / 2) * N);
+        const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
+        R[idx] = (t < m) ? __ldg(S.rec + (size_t)(i0 + t) * (RS / 2) + u) : make_double2(0.0, 0.0);
+    }
+    if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
+    if (tid <= N) sm.off[tid] = __ldg(S.off + tid);
+    TrackW<N> &W = sm.w[wi];
+    const bool inseg = lane < N * PPW;
+    const int q = inseg ? lane % PPW : 0, i = inseg ? lane / PPW : 0; // lane = i * PPW + q
+    const int seg0 = inseg ? q : PPW;
+    if (lane < PPW) {
+        W.done_path[lane] = -1;
+        W.cell[lane] = 0;
+        W.acc[lane] = 0;
+        trk_pop<N>(W, A, lane);
+    }
+    __syncthreads(); // tables and records
+    for (;;) {
+        // (1) write back finished paths, accept trial points, load new paths; the query point
+        double2 xv = make_double2(LOGS ? 0.0 : 1.0, 0.0);
+        if (inseg) {
+            if (W.acc[q]) W.xa[i][q] = W.xt[i][q];
+            if (W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
+            if (W.refill[q]) W.xa[i][q] = A.x[W.path[q] * N + i];
+            const int ph = W.phase[q];
+            if (ph == PH_CORRECT) xv = W.xt[i][q];
+            else if (ph != PH_IDLE) xv = W.xa[i][q];
+        }
+        __syncwarp();
+        if (lane < PPW) {
+            W.done_path[lane] = -1;
+            W.acc[lane] = 0;
+            W.refill[lane] = 0;
+            W.st[lane] = 0;
+            const int ph = W.phase[lane];
+            W.tau[lane] = (ph == PH_CORRECT) ? W.tau_t[lane] : ((ph == PH_PREDICT) ? W.tau_a[lane] : 0.0);
+        }
+        __syncwarp();
+        // (2) stage 1 for variable i, row i, solve (lane (i, q) ends with variable col)
+        {
+            double rho, th;
+            int st = 0;
+            if (LOGS) {
+                if (!(isfinite(xv.x) && isfinite(xv.y))) { st = PT_NONFINITE; rho = 0.0; th = 0.0; }
+                else {
+                    rho = xv.x;
+                    const double kq = rint(xv.y * INV_2PI); // wrap Im z into [-pi, pi] (integer a)
+                    th = fma(-kq, TWO_PI_LO, fma(-kq, TWO_PI_HI, xv.y));
+                }
+            } else {
+                double2 iv;
+                log_split(xv, rho, th, iv, st);
+            }
+            if (inseg) W.rt[i][q] = make_double2(rho, th);
+            if (st && inseg) atomicOr(&W.st[q], st);
+        }
+        __syncwarp();
+        {
+            double2 a[N + 2];
+            int e;
+            const double *wq = A.cellw ? A.cellw + (size_t)W.cell[q] * A.M : nullptr;
+            eval_row_tw<N>(sm, R, W, i, q, wq, a, e);
+            normalize_row<N>(a);
+            int col;
+            double2 dE, dN;
+            bool sing;
+            lsolve_regs<N, PPW, G::KS>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, inseg, col, dE, dN, sing);
+            if (inseg) {
+                if (sing) atomicOr(&W.st[q], PT_SINGULAR);
+                W.dd[col][q] = (W.phase[q] == PH_PREDICT) ? dE : dN;
+            }
+        }
+        __syncwarp();
+        // (3) element-parallel updates (lane (i, q): variable i of slot q)
+        if (inseg) {
+            const int ph = W.phase[q];
+            if (W.st[q] == 0 && ph != PH_IDLE) {
+                const double2 dl = W.dd[i][q];
+                if (ph == PH_PREDICT) {
+                    const double h = fmin(W.dt[q], -W.tau_a[q]);
+                    W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], dl, h)
+                                            : trk_update<N, LOGS>(W.xa[i][q], dl, h);
+                } else if (ph == PH_CORRECT) {
+                    const double2 v = W.xt[i][q];
+                    W.xt[i][q] = trk_update<N, LOGS>(v, dl, 1.0);
+                    W.nd2[i][q] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_i / x_i|^2 (reading R14)
+                } else { // FINAL
+                    const double2 v = W.xa[i][q];
+                    W.xa[i][q] = trk_update<N, LOGS>(v, dl, 1.0);
+                    W.nd2[i][q] = fma(dl.x, dl.x, dl.y * dl.y);
+                }
+            }
+        }
+        __syncwarp();
+        // (4) per-slot decisions
+        if (lane < PPW && W.phase[lane] != PH_IDLE) trk_decide<N, LOGS>(W, A, S, lane, W.st[lane]);
+        __syncwarp();
+        const bool busy = __any_sync(0xffffffffu, lane < PPW && W.phase[lane] != PH_IDLE);
+        if (!busy) {
+            if (inseg && W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
+            break;
+        }
+    }
+}
+
 #ifndef __CUDACC_RTC__
+// k_trackw: n <= 12, LU, affine systems, Euler predictor; PHT_TRACKW=0 selects k_track.
+template <int N>
+bool trackw_eligible(const DevSys &S, const TrackArgs &A)
+{
+    if (N > 12 || S.proj || A.solver != SOLVER_LU || A.o.predictor == 1 || S.mt <= 0) return false;
+    const char *ev = getenv("PHT_TRACKW");
+    return !(ev && ev[0] == '0');
+}
+
+template <int N, bool LOGS>
+cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+{
+    constexpr int PPW = GeoW<N>::PPW;
+    const size_t sb = ((sizeof(SmemTW<N>) + 15) & ~(size_t)15) + (size_t)S.mt * N * rec_stride(N) * sizeof(double);
+    if (sb > 200 * 1024) return cudaErrorNotSupported;
+    static std::atomic<int64_t> conf_sb[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if ((int64_t)sb > conf_sb[dev & 63].load()) {
+        cudaError_t e = cudaFuncSetAttribute(k_trackw<N, LOGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        if (e != cudaSuccess) return e;
+        conf_sb[dev & 63].store((int64_t)sb);
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trackw<N, LOGS>, GeoW<N>::NT, sb);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sms * per_sm;
+    const int64_t need = (A.P + (int64_t)PPW * GeoW<N>::WARPS - 1) / ((int64_t)PPW * GeoW<N>::WARPS);
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    k_trackw<N, LOGS><<<dim3((unsigned)grid), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
+    return cudaGetLastError();
+}
+
 template <int N, bool LOGS>
 cudaError_t launch_track_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
@@ -1844,6 +2089,11 @@ cudaError_t launch_track_t(const DevSys &S, const TrackArgs &A, cudaStream_t str
 template <int N>
 cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
+    if (trackw_eligible<N>(S, A)) {
+        const cudaError_t e = A.o.log_state ? launch_trackw_t<N, true>(S, A, stream, sms)
+                                            : launch_trackw_t<N, false>(S, A, stream, sms);
+        if (e != cudaErrorNotSupported) return e;
+    }
     return A.o.log_state ? launch_track_t<N, true>(S, A, stream, sms) : launch_track_t<N, false>(S, A, stream, sms);
 }
 
