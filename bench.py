@@ -341,6 +341,9 @@ TRACK_CONFIGS = [("katsura-10", 10_000, "BASELINE.json configs[1]: katsura-10 fu
                  ("cyclic-10", 1_000_000, "BASELINE.json configs[2]: cyclic-10 predictor-corrector tracking, sharded")]
 
 
+TRACK_REPS = 3
+
+
 def tracking_section(world, rank, dev, which):
     """Full path tracking of the stored start systems (log-coordinate state, device tracker).
     Each rank tracks its shard; ONE gather of endpoints/status/stats to rank 0 is inside the
@@ -370,19 +373,30 @@ def tracking_section(world, rank, dev, which):
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        st, stats = g.track_cells(zl, tl, wcell, cl)
-        if world > 1:
-            res = gather_to_rank0({"z": zl, "status": st, "stats": stats}, idx, Ptot)
-        else:
-            res = {"z": zl, "status": st, "stats": stats}
-        e1.record()
-        torch.cuda.synchronize(dev)
-        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        # TRACK_REPS independent runs from the same start points; the median is reported (one
+        # run of a few ms is exposed to run-to-run spread: DESIGN.md §3c)
+        runs = []
+        for r in range(TRACK_REPS):
+            zr, tr = zl.clone(), tl.clone()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st, stats = g.track_cells(zr, tr, wcell, cl)
+            if world > 1:
+                res = gather_to_rank0({"z": zr, "status": st, "stats": stats}, idx, Ptot)
+            else:
+                res = {"z": zr, "status": st, "stats": stats}
+            e1.record()
+            torch.cuda.synchronize(dev)
+            ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            runs.append(float(ms.item()))
+        zl = zr
+        ms = torch.tensor([float(np.median(runs))], dtype=torch.float64)
         if rank == 0:
             stv = res["status"].cpu().numpy()
             sts = res["stats"].cpu().numpy()
@@ -394,7 +408,8 @@ def tracking_section(world, rank, dev, which):
                          "lift_max": L, "ms": t, "paths_per_s": Ptot / (t * 1e-3), "status": hist,
                          "steps_mean": float(sts[:, 0].mean()), "steps_max": int(sts[:, 0].max()),
                          "evals": int(sts[:, 2].sum()), "evals_per_s": float(sts[:, 2].sum() / (t * 1e-3)),
-                         "state": "cell coordinates (pht_track_cells), log-chart Euler predictor, default opts"}
+                         "state": "cell coordinates (pht_track_cells), log-chart Euler predictor, default opts",
+                         "runs_ms": runs}
         if name == "cyclic-10":
             for proj in (False, True):
                 r2 = _second_stage(world, rank, dev, sysm, L, zl, st, proj)
