@@ -1,0 +1,130 @@
+"""The warp-per-group kernels (k_stepw, k_trackw) against the tile kernels
+(k_pht, k_track) on identical inputs, and the step against the oracle across the n range the
+warp kernels cover.  The row arithmetic and the Gauss-Jordan elimination are the same code in
+both layouts, so results agree to rounding; statuses and finite counts are identical.
+PHT_STEPW / PHT_TRACKW = 0 select the tile kernels (read at every launch)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from tests.parity import rel_err, skeel_cond
+from workloads import startsys as SS
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2111_14317_b200 as P
+    return P
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+SYS = {"cyclic-5": lambda: W.cyclic(5), "cyclic-7": lambda: W.cyclic(7, lift_max=100),
+       "cyclic-10": lambda: W.cyclic(10, lift_max=100), "katsura-10": lambda: W.katsura(10, lift_max=100),
+       "noon-10": lambda: W.noon(10, lift_max=100), "chandra-6": lambda: W.chandra(6),
+       "random-8x12": lambda: W.random_dense(8, 12), "n1": lambda: W.from_terms("n1", 1, [[((2,), 1.0), ((0,), -3.0)]])}
+
+
+@pytest.mark.parametrize("name,p,K", [("cyclic-5", 4099, 1), ("cyclic-7", 1001, 2), ("cyclic-10", 3001, 1),
+                                      ("katsura-10", 997, 2), ("noon-10", 1003, 1), ("chandra-6", 515, 3),
+                                      ("random-8x12", 333, 1), ("n1", 97, 2)])
+def test_stepw_equals_tile_kernel(P, name, p, K):
+    """Ragged batches (not a multiple of the points per warp or per CTA) and K = 1..3."""
+    sysm = SYS[name]()
+    g = P.System.from_workload(sysm)
+    x, _, tau = W.random_points(p, sysm.n, seed=31, tau_lo=-0.05)
+    dtau = _cuda(np.full(p, 0.01))
+    out = []
+    for m in ("1", "0"):
+        with _env(PHT_STEPW=m):
+            xg, tg = _cuda(x), _cuda(tau)
+            st, dn = g.pc_step(xg, tg, dtau, newton_iters=K)
+            out.append((xg.cpu().numpy(), tg.cpu().numpy(), st.cpu().numpy(), dn.cpu().numpy()))
+    (xw, tw, sw, dw), (xt, tt, stt, dt) = out
+    assert np.array_equal(sw, stt) and np.array_equal(tw, tt)
+    ok = sw == 0
+    assert ok.sum() >= 0.5 * p
+    assert rel_err(xw[ok], xt[ok]).max() <= 1e-12
+    assert np.allclose(dw[ok], dt[ok], rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("name,p", [("cyclic-7", 301), ("chandra-6", 200), ("random-8x12", 150)])
+def test_stepw_oracle_parity(P, name, p):
+    """k_stepw (the default for n <= 12) against the oracle's Euler-Newton step."""
+    sysm = SYS[name]()
+    o = oracle.Oracle(sysm)
+    x, _, tau = W.random_points(p, sysm.n, seed=32, tau_lo=-0.05)
+    dtau = np.full(p, 0.01)
+    xo, tauo, sto, dno = o.pc_step(x, tau, dtau, K=1)
+    g = P.System.from_workload(sysm)
+    xg, tg = _cuda(x), _cuda(tau)
+    st, dn = g.pc_step(xg, tg, _cuda(dtau), newton_iters=1)
+    xg, st = xg.cpu().numpy(), st.cpu().numpy()
+    assert np.array_equal(tg.cpu().numpy(), tauo)
+    cond = skeel_cond(o.evaluate(x, np.exp(tau))["Jx"])
+    well = (st == 0) & (sto == 0) & (cond <= 1e3)
+    assert well.sum() >= 0.5 * p
+    assert rel_err(xg[well], xo[well]).max() <= 1e-9
+
+
+def test_stepw_status_isolation(P):
+    """A zero coordinate, a non-finite x and a non-finite tau flag only their own points."""
+    sysm = W.cyclic(10, lift_max=100)
+    g = P.System.from_workload(sysm)
+    x, _, tau = W.random_points(64, 10, seed=33, tau_lo=-0.05)
+    x[5, 3] = 0
+    x[17, 0] = np.nan
+    tau[40] = np.inf
+    xg, tg = _cuda(x), _cuda(tau)
+    st, _ = g.pc_step(xg, tg, _cuda(np.full(64, 0.01)), newton_iters=1)
+    st = st.cpu().numpy()
+    bad = {5, 17, 40}
+    assert all(st[i] != 0 for i in bad)
+    assert np.sum(st[[i for i in range(64) if i not in bad]] != 0) <= 2
+
+
+@pytest.mark.parametrize("name,L", [("katsura-10", 10_000), ("cyclic-10", 1_000_000)])
+def test_trackw_equals_tile_tracker(P, name, L):
+    """Every start path of katsura-10 (990) / cyclic-10 (35,940): identical statuses and finite
+    counts, endpoints <= 1e-10 apart (an accept/reject decision may flip at rounding level,
+    reading R14 -- the endpoints then still agree to the tracking tolerance)."""
+    from workloads.make_starts import CONFIGS
+    sysm = CONFIGS[name](L)
+    cells = SS.load_cells(name, L)
+    z, tau0, ids = SS.start_points_cells(sysm, cells)
+    Wc = _cuda(SS.cell_lifts_fast(sysm, cells))
+    g = P.System.from_workload(sysm)
+    res = []
+    for m in ("1", "0"):
+        with _env(PHT_TRACKW=m):
+            zd, td = _cuda(z), _cuda(tau0)
+            st, stats = g.track_cells(zd, td, Wc, _cuda(ids))
+            res.append((zd.cpu().numpy(), st.cpu().numpy()))
+    (zw, sw), (zt, stt) = res
+    assert np.array_equal(sw, stt) and np.sum(sw == 0) == len(z)
+    xw, xt = np.exp(zw), np.exp(zt)
+    assert (np.linalg.norm(xw - xt, axis=1) / np.linalg.norm(xt, axis=1)).max() <= 1e-10
