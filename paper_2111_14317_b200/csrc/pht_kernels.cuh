@@ -1204,7 +1204,13 @@ struct GeoW {
     static constexpr int NT = WARPS * 32;
     static constexpr int RW = N + 2;
     static constexpr int KS = (N + 3) & ~3;
-    static constexpr int MINB = PHT_STEPW_MINB; // 16 warps per SM at <= 128 registers (4 x 4: -1%, 4 x 5: spills)
+    static constexpr int MINB = PHT_STEPW_MINB; // tracker: 16 warps per SM at <= 128 registers (4 x 4: -1%, 4 x 5: spills)
+    // the step kernel: one 16-warp CTA per SM (+2.7% on cyclic-10 over 2 x 8: one copy of the tables
+    // and records per SM); the tracker keeps 8-warp CTAs, which spread few paths over more SMs
+    // (katsura-10, 990 paths: 6.1 ms vs 7.5 ms with 16-warp CTAs)
+    static constexpr int SWARPS = 16;
+    static constexpr int SNT = SWARPS * 32;
+    static constexpr int SMINB = 1;
 };
 
 template <int N>
@@ -1219,7 +1225,7 @@ struct SmemW {
         double dn2[N][GeoW<N>::PPW];
         double tau[GeoW<N>::PPW];
         int st[GeoW<N>::PPW];
-    } w[GeoW<N>::WARPS];
+    } w[GeoW<N>::SWARPS];
     int mk[N]; // terms per equation
     // followed by the records R[MT][N][rec_stride(N) / 2] (double2)
 };
@@ -1286,7 +1292,7 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
 }
 
 template <int N>
-__global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_stepw(const DevSys S, const Args A, int MT)
+__global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const DevSys S, const Args A, int MT)
 {
     using G = GeoW<N>;
     constexpr int RS = rec_stride(N), PPW = G::PPW;
@@ -1294,8 +1300,8 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_stepw(const DevS
     SmemW<N> &sm = *reinterpret_cast<SmemW<N> *>(smem_raw);
     double2 *R = reinterpret_cast<double2 *>(smem_raw + ((sizeof(SmemW<N>) + 15) & ~(size_t)15));
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-    load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
-    for (int idx = tid; idx < MT * N * (RS / 2); idx += G::NT) { // records, term-major
+    load_tables(S, sm.exptab, sm.cistab, tid, G::SNT);
+    for (int idx = tid; idx < MT * N * (RS / 2); idx += G::SNT) { // records, term-major
         const int u = idx % (RS / 2), kk = (idx / (RS / 2)) % N, t = idx / ((RS / 2) * N);
         const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
         R[idx] = (t < m) ? __ldg(S.rec + (size_t)(i0 + t) * (RS / 2) + u) : make_double2(0.0, 0.0);
@@ -1309,7 +1315,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_stepw(const DevS
     const int q = inseg ? lane % PPW : 0, i = inseg ? lane / PPW : 0; // point of the group, index
     const int seg0 = inseg ? q : PPW;                                 // segment (PPW: no point)
     const int64_t groups = (A.P + PPW - 1) / PPW;
-    for (int64_t grp = (int64_t)blockIdx.x * G::WARPS + wi; grp < groups; grp += (int64_t)gridDim.x * G::WARPS) {
+    for (int64_t grp = (int64_t)blockIdx.x * G::SWARPS + wi; grp < groups; grp += (int64_t)gridDim.x * G::SWARPS) {
         const int64_t base = grp * PPW, gp = base + q;
         const bool act = inseg && gp < A.P;
         double2 xv = make_double2(1.0, 0.0); // lanes of points past P carry a harmless dummy
@@ -2184,12 +2190,12 @@ cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
     }
     int64_t fg = (last_sb[dev & 63].load() == (int64_t)sb) ? last_fg[dev & 63].load() : 0;
     if (fg == 0) {
-        fg = persistent_grid(reinterpret_cast<const void *>(k_stepw<N>), GeoW<N>::NT, sb);
+        fg = persistent_grid(reinterpret_cast<const void *>(k_stepw<N>), GeoW<N>::SNT, sb);
         last_fg[dev & 63].store(fg);
         last_sb[dev & 63].store((int64_t)sb);
     }
-    const int64_t need = (groups + GeoW<N>::WARPS - 1) / GeoW<N>::WARPS;
-    k_stepw<N><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
+    const int64_t need = (groups + GeoW<N>::SWARPS - 1) / GeoW<N>::SWARPS;
+    k_stepw<N><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoW<N>::SNT), sb, stream>>>(S, A, S.mt);
     return cudaGetLastError();
 }
 
