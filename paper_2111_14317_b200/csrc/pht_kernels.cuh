@@ -1224,6 +1224,7 @@ struct SmemW {
         alignas(16) unsigned keys[GeoW<N>::PPW * GeoW<N>::KS];
         double dn2[N][GeoW<N>::PPW];
         double tau[GeoW<N>::PPW];
+        double tinv[GeoW<N>::PPW];
         int st[GeoW<N>::PPW];
     } w[GeoW<N>::SWARPS];
     int mk[N]; // terms per equation
@@ -1291,9 +1292,14 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
     e = (int)acc.ed;
 }
 
-template <int N>
+// MODE_STEP: the Euler-Newton step in place; MODE_DIRS: the directions dE = dx/dt, dN at (x, t)
+// (pht_euler_newton) -- one evaluation and solve, dE and dN staged in the x and (rho, vartheta)
+// tiles (each lane overwrites only its own variable col, which no other lane reads any more).
+template <int N, int MODE>
 __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const DevSys S, const Args A, int MT)
 {
+    static_assert(MODE == MODE_DIRS || MODE == MODE_STEP, "k_stepw: directions or step");
+    constexpr bool DIRS = MODE == MODE_DIRS;
     using G = GeoW<N>;
     constexpr int RS = rec_stride(N), PPW = G::PPW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1319,12 +1325,19 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
         const int64_t base = grp * PPW, gp = base + q;
         const bool act = inseg && gp < A.P;
         double2 xv = make_double2(1.0, 0.0); // lanes of points past P carry a harmless dummy
-        if (act) xv = A.xio[gp * N + i];
+        if (act) xv = DIRS ? A.xin[gp * N + i] : A.xio[gp * N + i];
         if (lane < PPW) {
-            double tv = (base + lane < A.P) ? A.tauio[base + lane] : 0.0;
             int st = 0;
-            if (!isfinite(tv)) { st = PT_NONFINITE; tv = 0.0; }
-            W.tau[lane] = tv;
+            if (DIRS) { // t > 0 in, tau = log t
+                double tv = (base + lane < A.P) ? A.tin[base + lane] : 1.0;
+                if (!(tv > 0.0) || !isfinite(tv)) { st = PT_NONFINITE; tv = 1.0; }
+                W.tau[lane] = log(tv);
+                W.tinv[lane] = 1.0 / tv;
+            } else {
+                double tv = (base + lane < A.P) ? A.tauio[base + lane] : 0.0;
+                if (!isfinite(tv)) { st = PT_NONFINITE; tv = 0.0; }
+                W.tau[lane] = tv;
+            }
             W.st[lane] = st;
         }
         __syncwarp();
@@ -1341,18 +1354,26 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
             if (st && act) atomicOr(&W.st[q], st);
         }
         __syncwarp();
-        for (int it = 0; it <= A.K; ++it) {
+        const int iters = DIRS ? 1 : A.K + 1;
+        for (int it = 0; it < iters; ++it) {
             double2 a[N + 2];
             int e;
             eval_row_w<N>(sm, R, W, i, q, a, e); // row i of point q: [dh_i/dz | dh_i/dtau | h_i] 2^-e
             normalize_row<N>(a);
             __syncwarp(); // every lane has read tau and (rho, vartheta)
-            if (it == 0 && lane < PPW && base + lane < A.P) W.tau[lane] += A.dtau[base + lane];
+            if (!DIRS && it == 0 && lane < PPW && base + lane < A.P) W.tau[lane] += A.dtau[base + lane];
             int col;
             double2 dE, dN;
             bool sing;
             lsolve_regs<N, PPW, G::KS>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, act, col, dE, dN, sing);
-            if (act) { // the lane whose row pivoted column col updates variable col
+            if (act && DIRS) { // dx/dt = x (.) delta_E / t, dN_x = x (.) delta_N (Jx = G diag(1/x))
+                if (sing) atomicOr(&W.st[q], PT_SINGULAR);
+                const double2 xo = W.xs[col][q];
+                const double2 de = cmul(xo, dE), dn = cmul(xo, dN);
+                const double ti = W.tinv[q];
+                W.xs[col][q] = make_double2(de.x * ti, de.y * ti);
+                W.rt[col][q] = dn;
+            } else if (act) { // the lane whose row pivoted column col updates variable col
                 if (sing) atomicOr(&W.st[q], PT_SINGULAR);
                 const double2 xo = W.xs[col][q];
                 double2 xn;
@@ -1376,6 +1397,13 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
                 }
             }
             __syncwarp();
+        }
+        if (DIRS) {
+            if (act && A.dE) A.dE[gp * N + i] = W.xs[i][q];
+            if (act && A.dN) A.dN[gp * N + i] = W.rt[i][q];
+            if (lane < PPW && base + lane < A.P && A.status) A.status[base + lane] = (uint8_t)W.st[lane];
+            __syncwarp();
+            continue;
         }
         if (act) A.xio[gp * N + i] = W.xs[i][q];
         if (lane < PPW && base + lane < A.P) {
@@ -2171,7 +2199,7 @@ bool stepw_eligible(const DevSys &S, const Args &A)
     return !(ev && ev[0] == '0');
 }
 
-template <int N>
+template <int N, int MODE>
 cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
 {
     constexpr int PPW = GeoW<N>::PPW;
@@ -2184,18 +2212,18 @@ cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
     int dev = 0;
     cudaGetDevice(&dev);
     if ((int64_t)sb > conf_sb[dev & 63].load()) {
-        cudaError_t e = cudaFuncSetAttribute(k_stepw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        cudaError_t e = cudaFuncSetAttribute(k_stepw<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
         if (e != cudaSuccess) return e;
         conf_sb[dev & 63].store((int64_t)sb);
     }
     int64_t fg = (last_sb[dev & 63].load() == (int64_t)sb) ? last_fg[dev & 63].load() : 0;
     if (fg == 0) {
-        fg = persistent_grid(reinterpret_cast<const void *>(k_stepw<N>), GeoW<N>::SNT, sb);
+        fg = persistent_grid(reinterpret_cast<const void *>(k_stepw<N, MODE>), GeoW<N>::SNT, sb);
         last_fg[dev & 63].store(fg);
         last_sb[dev & 63].store((int64_t)sb);
     }
     const int64_t need = (groups + GeoW<N>::SWARPS - 1) / GeoW<N>::SWARPS;
-    k_stepw<N><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoW<N>::SNT), sb, stream>>>(S, A, S.mt);
+    k_stepw<N, MODE><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoW<N>::SNT), sb, stream>>>(S, A, S.mt);
     return cudaGetLastError();
 }
 
@@ -2206,10 +2234,14 @@ cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream
     switch (mode) {
     case MODE_EVAL_X: return launch_eval_mode<N, MODE_EVAL_X>(S, A, stream);
     case MODE_EVAL_Z: return launch_eval_mode<N, MODE_EVAL_Z>(S, A, stream);
-    case MODE_DIRS: return launch_mode<N, MODE_DIRS>(S, A, stream);
+    case MODE_DIRS: {
+        cudaError_t e = cudaErrorNotSupported;
+        if (stepw_eligible<N>(S, A)) e = launch_stepw<N, MODE_DIRS>(S, A, stream);
+        return e == cudaErrorNotSupported ? launch_mode<N, MODE_DIRS>(S, A, stream) : e;
+    }
     case MODE_STEP: {
         cudaError_t e = cudaErrorNotSupported;
-        if (stepw_eligible<N>(S, A)) e = launch_stepw<N>(S, A, stream);
+        if (stepw_eligible<N>(S, A)) e = launch_stepw<N, MODE_STEP>(S, A, stream);
         return e == cudaErrorNotSupported ? launch_mode<N, MODE_STEP>(S, A, stream) : e;
     }
     default: return cudaErrorInvalidValue;

@@ -128,3 +128,21 @@ def test_trackw_equals_tile_tracker(P, name, L):
     assert np.array_equal(sw, stt) and np.sum(sw == 0) == len(z)
     xw, xt = np.exp(zw), np.exp(zt)
     assert (np.linalg.norm(xw - xt, axis=1) / np.linalg.norm(xt, axis=1)).max() <= 1e-10
+
+
+@pytest.mark.parametrize("name,p", [("cyclic-5", 2051), ("cyclic-10", 1001), ("katsura-10", 333), ("n1", 65)])
+def test_stepw_directions_equal_tile_kernel(P, name, p):
+    """pht_euler_newton through k_stepw<N, DIRS> equals the tile kernel k_pht<N, DIRS>."""
+    sysm = SYS[name]()
+    g = P.System.from_workload(sysm)
+    x, t, _ = W.random_points(p, sysm.n, seed=34, tau_lo=-0.05)
+    out = []
+    for m in ("1", "0"):
+        with _env(PHT_STEPW=m):
+            dE, dN, st = g.euler_newton(_cuda(x), _cuda(t))
+            out.append((dE.cpu().numpy(), dN.cpu().numpy(), st.cpu().numpy()))
+    (ew, nw, sw), (et, nt, stt) = out
+    assert np.array_equal(sw, stt)
+    ok = sw == 0
+    assert ok.sum() >= 0.5 * p
+    assert rel_err(ew[ok], et[ok]).max() <= 1e-12 and rel_err(nw[ok], nt[ok]).max() <= 1e-12
