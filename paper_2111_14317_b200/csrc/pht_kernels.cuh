@@ -1195,19 +1195,19 @@ template <int N>
 struct GeoW {
     static constexpr int PPW = 32 / N; // points per warp
 #ifndef PHT_STEPW_WARPS
-#define PHT_STEPW_WARPS 8
+#define PHT_STEPW_WARPS 4
 #endif
 #ifndef PHT_STEPW_MINB
-#define PHT_STEPW_MINB 2
+#define PHT_STEPW_MINB 4
 #endif
     static constexpr int WARPS = PHT_STEPW_WARPS;
     static constexpr int NT = WARPS * 32;
     static constexpr int RW = N + 2;
     static constexpr int KS = (N + 3) & ~3;
-    static constexpr int MINB = PHT_STEPW_MINB; // tracker: 16 warps per SM at <= 128 registers (4 x 4: -1%, 4 x 5: spills)
+    static constexpr int MINB = PHT_STEPW_MINB; // tracker: 4 CTAs x 4 warps per SM at <= 128 registers
     // the step kernel: one 16-warp CTA per SM (+2.7% on cyclic-10 over 2 x 8: one copy of the tables
-    // and records per SM); the tracker keeps 8-warp CTAs, which spread few paths over more SMs
-    // (katsura-10, 990 paths: 6.1 ms vs 7.5 ms with 16-warp CTAs)
+    // and records per SM); the tracker uses 4-warp CTAs, which spread few paths over more SMs
+    // (katsura-10, 990 paths: 5.5 ms with 4-warp CTAs, 5.9 with 8, 7.5 with 16)
     static constexpr int SWARPS = 16;
     static constexpr int SNT = SWARPS * 32;
     static constexpr int SMINB = 1;
