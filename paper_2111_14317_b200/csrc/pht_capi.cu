@@ -463,7 +463,13 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     A.solver = s->solver;
     const bool evalm = mode == pht::MODE_EVAL_X || mode == pht::MODE_EVAL_Z;
     const unsigned need = evalm ? pht::JIT_EVAL : pht::JIT_STEP;
-    if (s->jit && (pht::jit_what(s->jit) & need)) {
+    // directions / step: from n = 10 on the generic warp-per-group kernel (k_stepw) is faster than
+    // the specialised tile kernel (cyclic-10 604 vs 487, noon-10 578 vs 492, katsura-10 356 vs 344 M
+    // evals/s); below n = 10 the specialised kernel stays ahead (cyclic-5 3080 vs 2760)
+    const bool warp_step = s->n >= 10 && s->n <= 12 && !s->proj && s->solver == PHT_SOLVER_LU;
+    const char *fj = getenv("PHT_JIT_STEP");
+    const bool jit_step = fj ? fj[0] == '1' : !warp_step;
+    if (s->jit && (pht::jit_what(s->jit) & need) && (evalm || jit_step)) {
         e = pht::jit_launch(s->jit, mode, S, A, st);
         if (e != cudaSuccess) return cuda_fail(e);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -741,8 +747,11 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     // than the generic kernel's, so few paths would run on few SMs (measured: 70 paths 4x slower)
     // (PHT_JIT_TRACK=1 forces it: tests)
     const char *force = getenv("PHT_JIT_TRACK");
+    // the warp-per-group tracker (k_trackw: n <= 12, LU, affine, Euler predictor) is faster than
+    // the specialised tile tracker, which is used only where k_trackw does not apply
+    const bool warp_track = s->n <= 12 && !s->proj && s->solver == PHT_SOLVER_LU && o.predictor != 1;
     if (s->jit && (pht::jit_what(s->jit) & pht::JIT_TRACK) &&
-        (p >= pht::jit_track_slots(s->jit, s->sms) || (force && force[0] == '1')))
+        ((!warp_track && p >= pht::jit_track_slots(s->jit, s->sms)) || (force && force[0] == '1')))
         e = pht::jit_launch_track(s->jit, S, A, st, s->sms);
     else switch (s->n) {
 #define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms); break;

@@ -24,6 +24,8 @@ def P():
 def _jit_tracker_always(monkeypatch):
     # the specialised tracker normally needs a full wave of paths; these small runs force it
     monkeypatch.setenv("PHT_JIT_TRACK", "1")
+    # and the specialised step kernels also where the warp-per-group kernel is the default
+    monkeypatch.setenv("PHT_JIT_STEP", "1")
 
 
 def _cuda(a):
