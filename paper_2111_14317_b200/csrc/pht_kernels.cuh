@@ -496,7 +496,7 @@ __device__ __forceinline__ double phi_of(const double (&a)[rec_stride(N)], const
 template <int N>
 struct RowAcc {
     double2 g[N], gt, h;
-    double ed, eh, el;
+    double ed; // row exponent; y = phi - ed ln2 with ln2 = LN2_HI + LN2_LO (ed LN2_HI exact)
 
     __device__ __forceinline__ void init(double phi0)
     {
@@ -505,17 +505,12 @@ struct RowAcc {
         gt = h = make_double2(0.0, 0.0);
         set_exp(rint(phi0 * KC[14]));
     }
-    __device__ __forceinline__ void set_exp(double e)
-    {
-        ed = e;
-        eh = e * KC[12];
-        el = e * KC[13];
-    }
-    __device__ __forceinline__ double reduced(double phi) const { return (phi - eh) - el; }
+    __device__ __forceinline__ void set_exp(double e) { ed = e; }
+    __device__ __forceinline__ double reduced(double phi) const { return fma(-ed, KC[13], fma(-ed, KC[12], phi)); }
     __device__ __forceinline__ double reduce(double phi)
     {
-        double y = (phi - eh) - el;
-        if (y > 512.0) { // rare: rescale everything to the new leading term (exact power of two)
+        double y = reduced(phi);
+        if (__builtin_expect(y > 512.0, 0)) { // rare: rescale everything to the new leading term (exact power of two)
             const double e2 = rint(phi * KC[14]);
             const double f = scalbn(1.0, (int)fmax(ed - e2, -2000.0));
 #pragma unroll
@@ -523,7 +518,7 @@ struct RowAcc {
             gt = make_double2(gt.x * f, gt.y * f);
             h = make_double2(h.x * f, h.y * f);
             set_exp(e2);
-            y = (phi - eh) - el;
+            y = reduced(phi);
         }
         return y;
     }
@@ -1208,7 +1203,10 @@ struct GeoW {
     // the step kernel: one 16-warp CTA per SM (+2.7% on cyclic-10 over 2 x 8: one copy of the tables
     // and records per SM); the tracker uses 4-warp CTAs, which spread few paths over more SMs
     // (katsura-10, 990 paths: 5.5 ms with 4-warp CTAs, 5.9 with 8, 7.5 with 16)
-    static constexpr int SWARPS = 16;
+#ifndef PHT_STEPW_SWARPS
+#define PHT_STEPW_SWARPS 16
+#endif
+    static constexpr int SWARPS = PHT_STEPW_SWARPS;
     static constexpr int SNT = SWARPS * 32;
     static constexpr int SMINB = 1;
 };
