@@ -260,7 +260,8 @@ def evaluation_section(world, rank, dev, reps=5):
                               "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak_tflops(1965.0),
                               "flops_per_point": fl / Pn},
                      "path": ("system-specialised point-per-thread kernel (NVRTC)" if spec_s is not None else
-                              "FP64 tensor cores (DMMA)" if g.dense else "scalar FP64 kernel")}
+                              "FP64 tensor cores (DMMA)" if (g.dense and n >= 11) else
+                              "warp-per-group kernel k_stepw<N, EVAL_X>" if n <= 10 else "scalar FP64 kernel")}
         if spec_s is not None:
             out[name]["specialize_s"] = spec_s
         del g, xd, td, H, J, Jt, st

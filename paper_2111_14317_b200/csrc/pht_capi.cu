@@ -475,7 +475,11 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return PHT_OK;
     }
-    const bool dense = s->dense && evalm;
+    // evaluation: the FP64 tensor-core kernel for n >= 11; up to n = 10 the warp-per-group kernel
+    // (k_stepw<N, EVAL_X>) is faster (cyclic-10 0.73 vs 0.62, noon-10 0.69 vs 0.61 G points/s;
+    // katsura-10, n = 11: 0.45 vs 0.58); PHT_DENSE=1 forces the tensor-core kernel
+    const char *fd = getenv("PHT_DENSE");
+    const bool dense = s->dense && evalm && (s->n >= 11 || (fd && fd[0] == '1') || mode == pht::MODE_EVAL_Z);
     const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff, s->max_ntk};
     switch (s->n) {
 #define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st); break;

@@ -1296,8 +1296,8 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
 template <int N, int MODE>
 __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const DevSys S, const Args A, int MT)
 {
-    static_assert(MODE == MODE_DIRS || MODE == MODE_STEP, "k_stepw: directions or step");
-    constexpr bool DIRS = MODE == MODE_DIRS;
+    static_assert(MODE == MODE_DIRS || MODE == MODE_STEP || MODE == MODE_EVAL_X, "k_stepw: modes");
+    constexpr bool DIRS = MODE == MODE_DIRS, EVAL = MODE == MODE_EVAL_X;
     using G = GeoW<N>;
     constexpr int RS = rec_stride(N), PPW = G::PPW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1323,10 +1323,10 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
         const int64_t base = grp * PPW, gp = base + q;
         const bool act = inseg && gp < A.P;
         double2 xv = make_double2(1.0, 0.0); // lanes of points past P carry a harmless dummy
-        if (act) xv = DIRS ? A.xin[gp * N + i] : A.xio[gp * N + i];
+        if (act) xv = (DIRS || EVAL) ? A.xin[gp * N + i] : A.xio[gp * N + i];
         if (lane < PPW) {
             int st = 0;
-            if (DIRS) { // t > 0 in, tau = log t
+            if (DIRS || EVAL) { // t > 0 in, tau = log t
                 double tv = (base + lane < A.P) ? A.tin[base + lane] : 1.0;
                 if (!(tv > 0.0) || !isfinite(tv)) { st = PT_NONFINITE; tv = 1.0; }
                 W.tau[lane] = log(tv);
@@ -1346,7 +1346,7 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
             log_split(xv, rho, th, iv, st); // a1 for variable i
             if (inseg) {
                 W.rt[i][q] = make_double2(rho, th);
-                W.xs[i][q] = xv;
+                W.xs[i][q] = EVAL ? iv : xv; // evaluation: 1/x_i for the diag(1/x) epilogue
                 W.dn2[i][q] = 0.0;
             }
             if (st && act) atomicOr(&W.st[q], st);
@@ -1357,6 +1357,29 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
             double2 a[N + 2];
             int e;
             eval_row_w<N>(sm, R, W, i, q, a, e); // row i of point q: [dh_i/dz | dh_i/dtau | h_i] 2^-e
+            if (EVAL) { // pht_evaluate: Jx_ij = G_ij / x_j, Jt = G_tau / t, H = h, row i
+                const double ti = W.tinv[q];
+                a[N] = make_double2(a[N].x * ti, a[N].y * ti);
+#pragma unroll
+                for (int j = 0; j < N; ++j) a[j] = cmul(a[j], W.xs[j][q]);
+                const bool scaled = A.rexp != nullptr;
+                if (!scaled) scale_row2<N + 2>(a, e);
+                bool fin = true;
+#pragma unroll
+                for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(a[c].x) && isfinite(a[c].y);
+                if (act) {
+                    if (!fin) atomicOr(&W.st[q], PT_NONFINITE);
+                    const int64_t r = gp * N + i;
+                    if (A.J) {
+#pragma unroll
+                        for (int j = 0; j < N; ++j) A.J[r * N + j] = a[j];
+                    }
+                    if (A.Jt) A.Jt[r] = a[N];
+                    if (A.H) A.H[r] = a[N + 1];
+                    if (scaled) A.rexp[r] = e;
+                }
+                break;
+            }
             normalize_row<N>(a);
             __syncwarp(); // every lane has read tau and (rho, vartheta)
             if (!DIRS && it == 0 && lane < PPW && base + lane < A.P) W.tau[lane] += A.dtau[base + lane];
@@ -1395,6 +1418,12 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
                 }
             }
             __syncwarp();
+        }
+        if (EVAL) {
+            __syncwarp();
+            if (lane < PPW && base + lane < A.P && A.status) A.status[base + lane] = (uint8_t)W.st[lane];
+            __syncwarp();
+            continue;
         }
         if (DIRS) {
             if (act && A.dE) A.dE[gp * N + i] = W.xs[i][q];
@@ -2197,6 +2226,15 @@ bool stepw_eligible(const DevSys &S, const Args &A)
     return !(ev && ev[0] == '0');
 }
 
+// pht_evaluate through k_stepw<N, EVAL_X>: affine systems, 6 <= n <= 12 (PHT_EVALW=0/1 overrides)
+template <int N>
+bool stepw_eval_eligible(const DevSys &S)
+{
+    const char *ev = getenv("PHT_EVALW");
+    if (ev) return ev[0] == '1' && N <= 12 && !S.proj && S.mt > 0;
+    return N >= 6 && N <= 12 && !S.proj && S.mt > 0;
+}
+
 template <int N, int MODE>
 cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
 {
@@ -2230,7 +2268,11 @@ template <int N>
 cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream)
 {
     switch (mode) {
-    case MODE_EVAL_X: return launch_eval_mode<N, MODE_EVAL_X>(S, A, stream);
+    case MODE_EVAL_X: {
+        cudaError_t e = cudaErrorNotSupported;
+        if (stepw_eval_eligible<N>(S)) e = launch_stepw<N, MODE_EVAL_X>(S, A, stream);
+        return e == cudaErrorNotSupported ? launch_eval_mode<N, MODE_EVAL_X>(S, A, stream) : e;
+    }
     case MODE_EVAL_Z: return launch_eval_mode<N, MODE_EVAL_Z>(S, A, stream);
     case MODE_DIRS: {
         cudaError_t e = cudaErrorNotSupported;
