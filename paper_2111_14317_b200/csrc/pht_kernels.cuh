@@ -2226,13 +2226,14 @@ bool stepw_eligible(const DevSys &S, const Args &A)
     return !(ev && ev[0] == '0');
 }
 
-// pht_evaluate through k_stepw<N, EVAL_X>: affine systems, 6 <= n <= 12 (PHT_EVALW=0/1 overrides)
+// pht_evaluate through k_stepw<N, EVAL_X>: affine systems, n <= 12 (cyclic-5 2.44 -> 3.24, cyclic-10
+// 0.59 -> 0.73 G points/s over the tile kernel k_phte); PHT_EVALW=0 selects k_phte
 template <int N>
 bool stepw_eval_eligible(const DevSys &S)
 {
     const char *ev = getenv("PHT_EVALW");
-    if (ev) return ev[0] == '1' && N <= 12 && !S.proj && S.mt > 0;
-    return N >= 6 && N <= 12 && !S.proj && S.mt > 0;
+    if (ev && ev[0] == '0') return false;
+    return N <= 12 && !S.proj && S.mt > 0;
 }
 
 template <int N, int MODE>

@@ -148,7 +148,7 @@ def test_stepw_directions_equal_tile_kernel(P, name, p):
     assert rel_err(ew[ok], et[ok]).max() <= 1e-12 and rel_err(nw[ok], nt[ok]).max() <= 1e-12
 
 
-@pytest.mark.parametrize("name,p", [("chandra-6", 517), ("cyclic-7", 1001), ("cyclic-10", 2003), ("noon-10", 301)])
+@pytest.mark.parametrize("name,p", [("cyclic-5", 777), ("chandra-6", 517), ("cyclic-7", 1001), ("cyclic-10", 2003), ("noon-10", 301), ("n1", 65)])
 def test_evaluate_warp_kernel_equals_tile_kernel(P, name, p):
     """pht_evaluate through k_stepw<N, EVAL_X> (the default for 6 <= n <= 10) equals the tile
     kernel k_phte, unscaled and with row exponents (the same row arithmetic)."""
