@@ -166,3 +166,27 @@ def test_evaluate_warp_kernel_equals_tile_kernel(P, name, p):
                 assert np.allclose(a, b, rtol=1e-13, atol=0) or np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-13
             else:
                 assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("m", [300, 420])
+def test_stepw_large_term_tables(P, m):
+    """Many terms per equation: the term records no longer fit the warp kernels' shared memory
+    (n = 6: 420 terms per equation) and the launch falls back to the tile kernel; just below the
+    limit (300 terms) k_stepw runs with one CTA per SM.  Both agree with the tile kernel."""
+    sysm = W.random_dense(6, m)
+    g = P.System.from_workload(sysm)
+    p = 301
+    x, t, tau = W.random_points(p, 6, seed=36, tau_lo=-0.05, rho_max=0.3)
+    out = []
+    for mm in ("1", "0"):
+        with _env(PHT_STEPW=mm, PHT_EVALW=mm):
+            xg, tg = _cuda(x), _cuda(tau)
+            st, _ = g.pc_step(xg, tg, _cuda(np.full(p, 0.01)), newton_iters=1)
+            H, Jx, Jt, est = g.evaluate(_cuda(x), _cuda(t))
+            out.append((xg.cpu().numpy(), st.cpu().numpy(), Jx.cpu().numpy(), est.cpu().numpy()))
+    (xw, sw, jw, ew), (xt, stt, jt, et) = out
+    assert np.array_equal(sw, stt) and np.array_equal(ew, et)
+    ok = sw == 0
+    assert ok.sum() >= 0.5 * p
+    assert rel_err(xw[ok], xt[ok]).max() <= 1e-11
+    assert np.max(np.abs(jw - jt)) <= 1e-12 * np.max(np.abs(jt))
