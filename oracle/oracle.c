@@ -612,6 +612,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+    if (final_iters < 1) return -1; /* as pht_track: at least one refinement iteration */
     const int pred_log = iopt[4];
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
@@ -677,20 +678,17 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             }
         }
         if (st == 0) {
-            /* refine at t = 1 until ||dN|| <= final_tol; an endpoint whose corrections only reach
-             * newton_tol within final_iters (the evaluation's accuracy floor at ill-conditioned
-             * endpoints) is accepted at that accuracy (reading R14) */
-            int conv = 0, solved = 1;
-            double nd = INFINITY;
+            /* refine at t = 1: up to final_iters Newton iterations until ||dN|| <= final_tol
+             * (SURVEY §8(c) O4 / ledger A24; componentwise relative norm, reading R14) */
+            int conv = 0;
             for (int it = 1; it <= final_iters; ++it) {
                 int s1 = solve_point(&s, xq, 1.0, 0, dN);
                 ++evals; ++fin;
-                if (s1) { solved = 0; break; }
-                nd = relmax(n, dN, xq);
+                if (s1) break;
+                const double nd = relmax(n, dN, xq);
                 for (int i = 0; i < 2 * n; ++i) xq[i] += dN[i];
                 if (nd <= final_tol) { conv = 1; break; }
             }
-            if (!conv && solved && nd <= newton_tol) conv = 1;
             double xinf = 0.0;
             for (int j = 0; j < n; ++j) xinf = fmax(xinf, cabs(load(xq + 2 * j)));
             st = (conv && xinf <= inf_norm) ? ORC_PT_OK : ORC_PT_DIVERGED;
@@ -789,6 +787,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+    if (final_iters < 1) return -1; /* as pht_track: at least one refinement iteration */
     const int pred_log = iopt[4];
     /* predictor 1: cubic Hermite extrapolation in the log chart through the previous and the
      * current accepted point and their Euler directions, log chart only */
@@ -885,17 +884,15 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
             }
         }
         if (st == 0) {
-            int conv = 0, solved = 1; /* final refinement: as orc_track (reading R14) */
-            double nd = INFINITY;
+            int conv = 0; /* final refinement to final_tol: as orc_track (ledger A24) */
             for (int it = 1; it <= final_iters; ++it) {
                 int s1 = solve_point_x(&s, xq, 0.0, wr, 0, dN);
                 ++evals; ++fin;
-                if (s1) { solved = 0; break; }
-                nd = relmax_d(n, dN);
+                if (s1) break;
+                const double nd = relmax_d(n, dN);
                 xupdate(n, xq, dN, 1.0);
                 if (nd <= final_tol) { conv = 1; break; }
             }
-            if (!conv && solved && nd <= newton_tol) conv = 1;
             double lmax = -INFINITY;
             for (int j = 0; j < n; ++j) lmax = fmax(lmax, xabs_log2(xq[j]));
             st = (conv && lmax <= log2(inf_norm)) ? ORC_PT_OK : ORC_PT_DIVERGED;
@@ -1082,6 +1079,7 @@ int orc_proj_track(int n, const int64_t *off, const int32_t *a, const double *c,
     const double shrink = opt[4], grow = opt[5], final_tol = opt[6], inf_norm = opt[7];
     const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
+    if (final_iters < 1) return -1; /* as pht_track: at least one refinement iteration */
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
         double *yq = y + 2 * m * q, E[130], N[130], yt[130];
