@@ -58,7 +58,11 @@ enum {
     PHT_PT_SINGULAR = 4,       /* |pivot| <= 1e-14 * (row max) in the direction solve       */
     PHT_PT_STEP_UNDERFLOW = 8, /* tracker: step size fell below dtau_min                    */
     PHT_PT_MAX_STEPS = 16,     /* tracker: step budget exhausted                            */
-    PHT_PT_DIVERGED = 32       /* tracker: endpoint not refined or ||x||_inf > inf_norm      */
+    PHT_PT_DIVERGED = 32,      /* tracker: endpoint not refined or ||x||_inf > inf_norm      */
+    PHT_PT_FLOOR = 64          /* tracker: finite endpoint whose final refinement reached only
+                                  newton_tol, not final_tol, within final_iters (the accuracy
+                                  floor of the log/exp evaluation, reading R30); the
+                                  endpoint is returned, counted apart from PHT_PT_OK            */
 };
 
 #define PHT_MAX_N 24     /* largest n with a compiled kernel                              */
@@ -112,8 +116,8 @@ int pht_homogenize(const pht_system *sys, int64_t p, const double *x, int32_t lo
 void pht_system_destroy(pht_system *sys);
 
 /* Query: n, number of packed terms M, largest equation size, owning device. */
-#define PHT_SYS_DENSE 1 /* evaluation uses the FP64 tensor-core (DMMA) path: n >= 10 and no zero
-                           coefficient dropped (env PHT_DENSE=0/1 overrides) */
+#define PHT_SYS_DENSE 1 /* the FP64 tensor-core (DMMA) evaluation tables exist: affine systems
+                           with n >= 10, or after pht_system_set_kernels(PHT_KERNELS_DENSE) */
 #define PHT_SYS_SPECIALIZED 2 /* system-specialised kernels loaded (pht_system_specialize) */
 #define PHT_SYS_PROJECTIVE 4  /* created by pht_system_create_projective */
 int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative pht_status */
@@ -132,7 +136,8 @@ int pht_system_flags(const pht_system *sys); /* PHT_SYS_* bits, or a negative ph
  * Host-synchronous; compile time grows with the number of terms (about 4 s for the n = 10
  * benchmark systems; images are cached per process by generated source).  Calling it again with
  * a subset of the compiled kernels is a no-op.  The tracker uses the specialised kernel only
- * when the batch fills at least one wave of its (larger) tiles; env PHT_JIT_TRACK=1 forces it.
+ * when the batch fills at least one wave of its (larger) tiles (pht_system_set_kernels(
+ * PHT_KERNELS_SPECIALIZED) forces the specialised kernels on every entry point they implement).
  * Returns PHT_OK, PHT_EJIT (NVRTC failed: log in pht_last_cuda_error), PHT_ECUDA (load failed),
  * PHT_EUNSUPPORTED (the generated code would exceed sum_terms (nnz(a) + 8) > 8000 units, e.g.
  * random dense 20 x 50: minutes of compile time and instruction-cache bound; such systems keep
@@ -172,6 +177,34 @@ int pht_system_info(const pht_system *sys, int32_t *n, int64_t *M, int32_t *max_
 #define PHT_SOLVER_LU 0
 #define PHT_SOLVER_QR 1
 int pht_system_set_solver(pht_system *sys, int32_t solver);
+
+/*
+ * Kernel family used by every entry point on this handle (explicit selection; results of all
+ * families agree to rounding, tests/test_gpu_warp_kernels.py, tests/test_gpu_parity.py):
+ *   PHT_KERNELS_AUTO (default)  the measured-best family per entry point and n:
+ *        evaluation: specialised kernels if loaded, FP64 tensor cores for n >= 11 (and
+ *        pht_evaluate_log from n = 10), else the warp-per-group kernel (n <= 12) or the tile
+ *        kernel; directions / step / tracking: warp-per-group kernels (n <= 12, LU, affine, Euler
+ *        predictor), the specialised kernels where those do not apply, else the tile kernels.
+ *   PHT_KERNELS_TILE            tile kernels (k_phte, k_pht, k_track) for every entry point.
+ *   PHT_KERNELS_WARP            warp-per-group kernels (k_stepw, k_trackw) wherever they apply,
+ *                               AUTO elsewhere (same as AUTO without specialised kernels).
+ *   PHT_KERNELS_DENSE           pht_evaluate / pht_evaluate_log on the FP64 tensor cores (builds the
+ *                               tables on first selection; PHT_EUNSUPPORTED for projective
+ *                               systems); AUTO for the other entry points.
+ *   PHT_KERNELS_SPECIALIZED     the system-specialised kernels for every entry point they were
+ *                               compiled for (PHT_EUNSUPPORTED before pht_system_specialize).
+ * Host-synchronous (PHT_KERNELS_DENSE may upload tables); not synchronised with calls in flight.
+ * Returns PHT_OK, PHT_EINVAL, PHT_EUNSUPPORTED, PHT_ENOMEM or PHT_ECUDA.  pht_system_kernels
+ * returns the current family.
+ */
+#define PHT_KERNELS_AUTO 0
+#define PHT_KERNELS_TILE 1
+#define PHT_KERNELS_WARP 2
+#define PHT_KERNELS_DENSE 3
+#define PHT_KERNELS_SPECIALIZED 4
+int pht_system_set_kernels(pht_system *sys, int32_t family);
+int pht_system_kernels(const pht_system *sys);
 
 /*
  * Batched evaluation of H, dH/dx, dH/dt (§5, Alg. 2).
@@ -248,9 +281,12 @@ int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
  *   opts    options; NULL = defaults (pht_track_opts_default).
  *   stats   int64[p][4] or NULL: accepted steps, rejected steps, evaluations (each one
  *           evaluate + 2-RHS solve), final Newton iterations.
- *   status  uint8[p]: PHT_PT_OK = finite converged endpoint; PHT_PT_SINGULAR,
+ *   status  uint8[p]: PHT_PT_OK = finite endpoint refined to final_tol; PHT_PT_FLOOR = finite
+ *           endpoint refined only to newton_tol (accuracy floor, counted apart); PHT_PT_SINGULAR,
  *           PHT_PT_STEP_UNDERFLOW, PHT_PT_MAX_STEPS, PHT_PT_DIVERGED (refinement failed or
  *           ||x||_inf > inf_norm), PHT_PT_NONFINITE (non-finite tau0).
+ * PHT_EINVAL for non-positive step sizes, shrink outside (0, 1), grow < 1, newton_iters,
+ * grow_after, max_steps or final_iters < 1.
  * Asynchronous on `stream`; uses a stream-ordered 8-byte device counter.
  */
 typedef struct {
@@ -265,7 +301,7 @@ typedef struct {
     int32_t newton_iters; /* 4    max corrector iterations per step (K)                  */
     int32_t grow_after;   /* 3                                                           */
     int32_t max_steps;    /* 10000                                                       */
-    int32_t final_iters;  /* 5                                                           */
+    int32_t final_iters;  /* 5    (>= 1)                                                  */
     int32_t log_state;    /* 0: x holds points x; 1: x holds z = log x (any branch) — for start
                              points far outside double range (|Re z| > ~700); the steps are the
                              same affine updates, applied as z <- z + log(1 + dx/x)            */
@@ -317,7 +353,7 @@ const char *pht_strerror(int code);
 const char *pht_last_cuda_error(void);
 
 /* ABI version (incremented on any signature change). */
-int pht_version(void);
+int pht_version(void); /* 2: pht_system_set_kernels, PHT_PT_FLOOR */
 
 #ifdef __cplusplus
 }

@@ -5,7 +5,7 @@ The CUDA library (lib/libpht.so) is required; importing this package without it 
 """
 from ._lib import PhtError, load as _load_lib  # noqa: F401
 from ._lib import (PT_OK, PT_ZERO_COORD, PT_NONFINITE, PT_SINGULAR, PT_STEP_UNDERFLOW,  # noqa: F401
-                   PT_MAX_STEPS, PT_DIVERGED, PHT_MAX_N)
+                   PT_MAX_STEPS, PT_DIVERGED, PT_FLOOR, PHT_MAX_N)
 
 _load_lib()
 

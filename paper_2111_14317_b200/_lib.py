@@ -15,10 +15,11 @@ LIB_PATH = os.environ.get("PHT_LIB") or os.path.join(_HERE, "lib", "libpht.so")
 
 PHT_MAX_N = 24
 PT_OK, PT_ZERO_COORD, PT_NONFINITE, PT_SINGULAR = 0, 1, 2, 4
-PT_STEP_UNDERFLOW, PT_MAX_STEPS, PT_DIVERGED = 8, 16, 32
+PT_STEP_UNDERFLOW, PT_MAX_STEPS, PT_DIVERGED, PT_FLOOR = 8, 16, 32, 64
 SYS_DENSE, SYS_SPECIALIZED, SYS_PROJECTIVE = 1, 2, 4
 SPEC_EVAL, SPEC_STEP, SPEC_TRACK, SPEC_ALL = 1, 2, 4, 7
 SOLVER_LU, SOLVER_QR = 0, 1
+KERNELS = {"auto": 0, "tile": 1, "warp": 2, "dense": 3, "specialized": 4}   # PHT_KERNELS_*
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -41,6 +42,8 @@ SIGNATURES = {
     "pht_track": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_track_cells": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pht_system_set_solver": (ctypes.c_int, [_vp, _i32]),
+    "pht_system_set_kernels": (ctypes.c_int, [_vp, _i32]),
+    "pht_system_kernels": (ctypes.c_int, [_vp]),
     "pht_system_specialize": (ctypes.c_int, [_vp, _i32]),
     "pht_specialize_compile": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
     "pht_specialize_source": (_i64, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64]),

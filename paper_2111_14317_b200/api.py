@@ -64,6 +64,17 @@ class System:
         check(self._lib.pht_system_set_solver(self._h, code), "pht_system_set_solver")
         return self
 
+    def set_kernels(self, family: str = "auto"):
+        """pht_system_set_kernels: 'auto' (measured-best, default), 'tile', 'warp', 'dense' (FP64
+        tensor-core evaluation) or 'specialized' (after specialize())."""
+        check(self._lib.pht_system_set_kernels(self._h, _lib.KERNELS[family]), "pht_system_set_kernels")
+        return self
+
+    @property
+    def kernels(self) -> str:
+        code = int(self._lib.pht_system_kernels(self._h))
+        return {v: k for k, v in _lib.KERNELS.items()}[code]
+
     def specialize(self, what: int = _lib.SPEC_ALL):
         """pht_system_specialize: compile and load the system-specialised kernels (NVRTC)."""
         check(self._lib.pht_system_specialize(self._h, int(what)), "pht_system_specialize")
@@ -169,9 +180,20 @@ class System:
                      status: np.ndarray = None, dn_norm: np.ndarray = None):
         """pht_pc_step_host on host numpy buffers (x, tau updated in place; pass pinned buffers,
         including status/dn_norm, for copy/compute overlap)."""
+        def host(a, dt, shape, what):
+            if not (isinstance(a, np.ndarray) and a.dtype == dt and a.shape == shape and a.flags.c_contiguous):
+                raise PhtError(f"{what} must be a C-contiguous numpy {np.dtype(dt).name} array of shape {shape}")
+            return a
+        if not isinstance(x, np.ndarray) or x.ndim != 2:
+            raise PhtError("x must be a numpy complex128 array [p, n]")
         p = x.shape[0]
-        st = status if status is not None else np.empty(p, np.uint8)
-        dn = dn_norm if dn_norm is not None else np.empty(p, np.float64)
+        host(x, np.complex128, (p, self.n), "x")
+        host(tau, np.float64, (p,), "tau")
+        host(dtau, np.float64, (p,), "dtau")
+        st = host(status, np.uint8, (p,), "status") if status is not None else np.empty(p, np.uint8)
+        dn = host(dn_norm, np.float64, (p,), "dn_norm") if dn_norm is not None else np.empty(p, np.float64)
+        if not x.flags.writeable or not tau.flags.writeable:
+            raise PhtError("x and tau are updated in place: they must be writeable")
         d = self._dev()
         check(self._lib.pht_pc_step_host(self._h, p, x.ctypes.data_as(ctypes.c_void_p),
                                          tau.ctypes.data_as(ctypes.c_void_p), dtau.ctypes.data_as(ctypes.c_void_p),

@@ -2,7 +2,7 @@
 #include "pht_dense.cuh"
 #include "pht_kernels.cuh"
 namespace pht {
-template cudaError_t launch<6>(int, const DevSys &, const Args &, cudaStream_t);
-template cudaError_t launch_track<6>(const DevSys &, const TrackArgs &, cudaStream_t, int);
+template cudaError_t launch<6>(int, const DevSys &, const Args &, cudaStream_t, int);
+template cudaError_t launch_track<6>(const DevSys &, const TrackArgs &, cudaStream_t, int, int);
 template cudaError_t launch_dense<6>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t);
 }

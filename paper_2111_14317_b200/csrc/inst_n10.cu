@@ -2,7 +2,7 @@
 #include "pht_dense.cuh"
 #include "pht_kernels.cuh"
 namespace pht {
-template cudaError_t launch<10>(int, const DevSys &, const Args &, cudaStream_t);
-template cudaError_t launch_track<10>(const DevSys &, const TrackArgs &, cudaStream_t, int);
+template cudaError_t launch<10>(int, const DevSys &, const Args &, cudaStream_t, int);
+template cudaError_t launch_track<10>(const DevSys &, const TrackArgs &, cudaStream_t, int, int);
 template cudaError_t launch_dense<10>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t);
 }

@@ -2,7 +2,7 @@
 #include "pht_dense.cuh"
 #include "pht_kernels.cuh"
 namespace pht {
-template cudaError_t launch<19>(int, const DevSys &, const Args &, cudaStream_t);
-template cudaError_t launch_track<19>(const DevSys &, const TrackArgs &, cudaStream_t, int);
+template cudaError_t launch<19>(int, const DevSys &, const Args &, cudaStream_t, int);
+template cudaError_t launch_track<19>(const DevSys &, const TrackArgs &, cudaStream_t, int, int);
 template cudaError_t launch_dense<19>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t);
 }

@@ -20,8 +20,8 @@
 
 namespace pht {
 #define PHT_DECL(N)                                                                             \
-    extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t);     \
-    extern template cudaError_t launch_track<N>(const DevSys &, const TrackArgs &, cudaStream_t, int); \
+    extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t, int); \
+    extern template cudaError_t launch_track<N>(const DevSys &, const TrackArgs &, cudaStream_t, int, int); \
     extern template cudaError_t launch_dense<N>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t);
 PHT_DECL(1) PHT_DECL(2) PHT_DECL(3) PHT_DECL(4) PHT_DECL(5) PHT_DECL(6) PHT_DECL(7) PHT_DECL(8)
 PHT_DECL(9) PHT_DECL(10) PHT_DECL(11) PHT_DECL(12) PHT_DECL(13) PHT_DECL(14) PHT_DECL(15)
@@ -41,6 +41,7 @@ struct pht_system {
     int dropped = 0; // terms with c = 0 removed by the packer
     int solver = 0;  // PHT_SOLVER_LU / PHT_SOLVER_QR (pht_system_set_solver)
     int proj = 0;    // projective system: n = n_eq + 1 homogeneous coordinates
+    int kernels = 0; // PHT_KERNELS_* (pht_system_set_kernels)
     double2 *d_rec = nullptr;
     int *d_off = nullptr;
     double *d_exptab = nullptr;
@@ -53,9 +54,12 @@ struct pht_system {
     // packed tables on the host (input of the code generator, pht_system_specialize)
     std::vector<double> h_rec;
     std::vector<int> h_off;
-    // system-specialised kernels (pht_jit.cu), or nullptr
+    // system-specialised kernels (pht_jit.cu), or nullptr; replaced only under jit_mu, read by
+    // the launchers under jit_mu (a snapshot); a replaced image stays loaded until destroy
+    // (launches queued on streams may still use it)
     std::mutex jit_mu;
     pht::JitKernels *jit = nullptr;
+    std::vector<pht::JitKernels *> jit_old;
     // workspace and copy/compute streams of the *_host entry points
     std::mutex ws_mu;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
@@ -157,6 +161,80 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
     return PHT_OK;
 }
 
+// FP64 tensor-core tables (pht_dense.cuh) from the packed records [a, omega, log|c|, arg c]:
+// B operands pre-swizzled into mma.m8n8k4 fragment order, one segment of n-tiles (8 terms) per
+// equation.  Stage 2: B = [A; omega; log|c|] (phi) and [A; 0; arg c] (theta), K = n + 2 padded
+// to 4; stage 4: B = [A_k | omega | 1] per 4-term half tile.
+static int build_dense(pht_system *s)
+{
+    if (s->dense) return PHT_OK;
+    const int n = s->n, RS = pht::rec_stride(n);
+    const std::vector<double> &rec = s->h_rec;
+    const std::vector<int> &off = s->h_off;
+    const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;
+    std::vector<int> ntoff(n + 1, 0);
+    int max_ntk = 0;
+    for (int k = 0; k < n; ++k) {
+        ntoff[k + 1] = ntoff[k] + (off[k + 1] - off[k] + 7) / 8;
+        max_ntk = std::max(max_ntk, ntoff[k + 1] - ntoff[k]);
+    }
+    const int NT = ntoff[n];
+    std::vector<double> b2p((size_t)NT * KS * 32), b2t((size_t)NT * KS * 32), b4((size_t)2 * NT * CT * 32);
+    for (int k = 0; k < n; ++k) {
+        for (int t = 0; t < ntoff[k + 1] - ntoff[k]; ++t) {
+            const int ntg = ntoff[k] + t;
+            for (int lane = 0; lane < 32; ++lane) {
+                const int g = lane >> 2, r = lane & 3;
+                const int64_t i = off[k] + 8 * t + g; // stage 2: B[r][g] = term 8t+g
+                const bool real = i < off[k + 1];
+                const double *ri = rec.data() + (size_t)i * RS;
+                for (int kk = 0; kk < KS; ++kk) {
+                    const int kr = 4 * kk + r;
+                    double vp = 0.0, vt = 0.0;
+                    if (real) {
+                        if (kr < n) vp = vt = ri[kr];
+                        else if (kr == n) vp = ri[n];
+                        else if (kr == n + 1) { vp = ri[n + 1]; vt = ri[n + 2]; }
+                    } else if (kr == n + 1) {
+                        vp = -1e300; // padding term: exp -> 0
+                    }
+                    b2p[((size_t)ntg * KS + kk) * 32 + lane] = vp;
+                    b2t[((size_t)ntg * KS + kk) * 32 + lane] = vt;
+                }
+                for (int h = 0; h < 2; ++h) { // stage 4: B[r][g] = term 8t+4h+r, column 8ct+g
+                    const int64_t i4 = off[k] + 8 * t + 4 * h + r;
+                    for (int ct = 0; ct < CT; ++ct) {
+                        const int c = 8 * ct + g;
+                        double v = 0.0;
+                        if (i4 < off[k + 1]) {
+                            const double *r4 = rec.data() + (size_t)i4 * RS;
+                            if (c < n) v = r4[c];
+                            else if (c == n) v = r4[n];
+                            else if (c == n + 1) v = 1.0;
+                        }
+                        b4[((size_t)(2 * ntg + h) * CT + ct) * 32 + lane] = v;
+                    }
+                }
+            }
+        }
+    }
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    cudaError_t e;
+    if ((e = cudaMalloc(&s->d_b2phi, b2p.size() * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_b2th, b2t.size() * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_b4, b4.size() * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_ntoff, ntoff.size() * sizeof(int))) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_b2phi, b2p.data(), b2p.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_b2th, b2t.data(), b2t.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_b4, b4.data(), b4.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_ntoff, ntoff.data(), ntoff.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
+    s->max_ntk = max_ntk;
+    s->dense = 1;
+    return PHT_OK;
+}
+
 static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const int32_t *exps, const double *coeffs,
                        const double *lifting, int32_t device, pht_system **out, bool proj)
 {
@@ -218,69 +296,14 @@ static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const in
         pht_system_destroy(s);
         return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
     }
-    // tensor-core evaluation policy: every system with n >= 10 (measured faster than the scalar
-    // kernel from n = 10 on, dense or sparse: profiles/r01_dense_tuning.txt); PHT_DENSE=0/1 overrides
-    {
-        int want = (n >= 10 && n_dropped == 0 && !proj) ? 1 : 0;
-        if (const char *ev = getenv("PHT_DENSE")) want = (ev[0] == '1') && n_dropped == 0 && !proj;
-        if (want) {
-            const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;
-            std::vector<int> ntoff(n + 1, 0);
-            for (int k = 0; k < n; ++k) {
-                ntoff[k + 1] = ntoff[k] + (int)((off[k + 1] - off[k] + 7) / 8);
-                s->max_ntk = std::max(s->max_ntk, ntoff[k + 1] - ntoff[k]);
-            }
-            const int NT = ntoff[n];
-            std::vector<double> b2p((size_t)NT * KS * 32), b2t((size_t)NT * KS * 32), b4((size_t)2 * NT * CT * 32);
-            for (int k = 0; k < n; ++k) {
-                for (int t = 0; t < ntoff[k + 1] - ntoff[k]; ++t) {
-                    const int ntg = ntoff[k] + t;
-                    for (int lane = 0; lane < 32; ++lane) {
-                        const int g = lane >> 2, r = lane & 3;
-                        const int64_t i = off[k] + 8 * t + g; // stage 2: B[r][g] = term 8t+g
-                        const bool real = i < off[k + 1];
-                        for (int kk = 0; kk < KS; ++kk) {
-                            const int kr = 4 * kk + r;
-                            double vp = 0.0, vt = 0.0;
-                            if (real) {
-                                const double cr = coeffs[2 * i], ci = coeffs[2 * i + 1];
-                                if (kr < n) vp = vt = exps[i * n + kr];
-                                else if (kr == n) vp = lifting[i];
-                                else if (kr == n + 1) { vp = std::log(std::hypot(cr, ci)); vt = std::atan2(ci, cr); }
-                            } else if (kr == n + 1) {
-                                vp = -1e300; // padding term: exp -> 0
-                            }
-                            b2p[((size_t)ntg * KS + kk) * 32 + lane] = vp;
-                            b2t[((size_t)ntg * KS + kk) * 32 + lane] = vt;
-                        }
-                        for (int h = 0; h < 2; ++h) { // stage 4: B[r][g] = term 8t+4h+r, column 8ct+g
-                            const int64_t i4 = off[k] + 8 * t + 4 * h + r;
-                            for (int ct = 0; ct < CT; ++ct) {
-                                const int c = 8 * ct + g;
-                                double v = 0.0;
-                                if (i4 < off[k + 1]) {
-                                    if (c < n) v = exps[i4 * n + c];
-                                    else if (c == n) v = lifting[i4];
-                                    else if (c == n + 1) v = 1.0;
-                                }
-                                b4[((size_t)(2 * ntg + h) * CT + ct) * 32 + lane] = v;
-                            }
-                        }
-                    }
-                }
-            }
-            if ((e = cudaMalloc(&s->d_b2phi, b2p.size() * 8)) != cudaSuccess ||
-                (e = cudaMalloc(&s->d_b2th, b2t.size() * 8)) != cudaSuccess ||
-                (e = cudaMalloc(&s->d_b4, b4.size() * 8)) != cudaSuccess ||
-                (e = cudaMalloc(&s->d_ntoff, ntoff.size() * sizeof(int))) != cudaSuccess ||
-                (e = cudaMemcpy(s->d_b2phi, b2p.data(), b2p.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
-                (e = cudaMemcpy(s->d_b2th, b2t.data(), b2t.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
-                (e = cudaMemcpy(s->d_b4, b4.data(), b4.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
-                (e = cudaMemcpy(s->d_ntoff, ntoff.data(), ntoff.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess) {
-                pht_system_destroy(s);
-                return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
-            }
-            s->dense = 1;
+    // tensor-core evaluation tables: built for every affine system with n >= 10 (the AUTO policy
+    // evaluates with DMMA from n = 11, profiles/r01_dense_tuning.txt), on demand otherwise
+    // (pht_system_set_kernels(PHT_KERNELS_DENSE))
+    if (n >= 10 && !proj) {
+        const int rc = build_dense(s);
+        if (rc != PHT_OK) {
+            pht_system_destroy(s);
+            return rc;
         }
     }
     *out = s;
@@ -320,6 +343,7 @@ extern "C" void pht_system_destroy(pht_system *s)
     }
     if (s->hev0) cudaEventDestroy(s->hev0);
     pht::jit_free(s->jit);
+    for (pht::JitKernels *J : s->jit_old) pht::jit_free(J);
     delete s;
 }
 
@@ -348,6 +372,30 @@ extern "C" int pht_system_set_solver(pht_system *s, int32_t solver)
     if (!s || (solver != PHT_SOLVER_LU && solver != PHT_SOLVER_QR)) return PHT_EINVAL;
     s->solver = solver;
     return PHT_OK;
+}
+
+extern "C" int pht_system_set_kernels(pht_system *s, int32_t family)
+{
+    if (!s || family < PHT_KERNELS_AUTO || family > PHT_KERNELS_SPECIALIZED) return PHT_EINVAL;
+    if (family == PHT_KERNELS_DENSE) {
+        if (s->proj) return PHT_EUNSUPPORTED;
+        const int rc = build_dense(s);
+        if (rc != PHT_OK) return rc;
+    }
+    if (family == PHT_KERNELS_SPECIALIZED) {
+        std::lock_guard<std::mutex> lk(s->jit_mu);
+        if (!s->jit) return PHT_EUNSUPPORTED;
+    }
+    s->kernels = family;
+    return PHT_OK;
+}
+
+extern "C" int pht_system_kernels(const pht_system *s) { return s ? s->kernels : PHT_EINVAL; }
+
+static pht::JitKernels *jit_snapshot(const pht_system *s)
+{
+    std::lock_guard<std::mutex> lk(const_cast<pht_system *>(s)->jit_mu);
+    return s->jit;
 }
 
 // System-specialised kernels (pht_jit.cu): generate, compile (NVRTC, sm_100a), load.
@@ -405,7 +453,8 @@ extern "C" int pht_system_specialize(pht_system *s, int32_t what)
     cudaError_t e = cudaSuccess;
     pht::JitKernels *J = pht::jit_load(s->n, (unsigned)what, cubin, names, &e);
     if (!J) return cuda_fail(e);
-    pht::jit_free(s->jit);
+    // the previous image may still be referenced by queued launches: unload it at destroy
+    if (s->jit) s->jit_old.push_back(s->jit);
     s->jit = J;
     return PHT_OK;
 }
@@ -451,6 +500,15 @@ extern "C" int64_t pht_specialize_source(int32_t n_eq, int32_t n_var, const int6
     return (int64_t)src.size() + 1;
 }
 
+// Kernel choice per entry point (family = PHT_KERNELS_*, pht_system_set_kernels).  AUTO, the
+// measured-best policy (DESIGN.md §3b/§3c, profiles/r01_dense_tuning.txt, r01_specialize.txt):
+//   evaluation   specialised kernels if loaded; FP64 tensor cores (k_dense) for n >= 11 and for
+//                pht_evaluate_log when the dense tables exist (n >= 10); else k_stepw<N, EVAL_X>
+//                (n <= 12) or the tile kernel k_phte
+//   directions / step   k_stepw for 10 <= n <= 12 (cyclic-10 604 vs 487 specialised, noon-10 578
+//                vs 492, katsura-10 356 vs 344 M evals/s); the specialised tile kernel below n = 10
+//                when loaded (cyclic-5 3080 vs 2760); else k_stepw (n <= 12) or k_pht
+// A forced family applies wherever it implements the entry point, AUTO elsewhere.
 static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *stream)
 {
     if (A0.P == 0) return PHT_OK;
@@ -461,28 +519,33 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     cudaError_t e;
     pht::Args A = A0;
     A.solver = s->solver;
+    const int fam = s->kernels;
     const bool evalm = mode == pht::MODE_EVAL_X || mode == pht::MODE_EVAL_Z;
     const unsigned need = evalm ? pht::JIT_EVAL : pht::JIT_STEP;
-    // directions / step: from n = 10 on the generic warp-per-group kernel (k_stepw) is faster than
-    // the specialised tile kernel (cyclic-10 604 vs 487, noon-10 578 vs 492, katsura-10 356 vs 344 M
-    // evals/s); below n = 10 the specialised kernel stays ahead (cyclic-5 3080 vs 2760)
     const bool warp_step = s->n >= 10 && s->n <= 12 && !s->proj && s->solver == PHT_SOLVER_LU;
-    const char *fj = getenv("PHT_JIT_STEP");
-    const bool jit_step = fj ? fj[0] == '1' : !warp_step;
-    if (s->jit && (pht::jit_what(s->jit) & need) && (evalm || jit_step)) {
-        e = pht::jit_launch(s->jit, mode, S, A, st);
+    pht::JitKernels *J = jit_snapshot(s);
+    const bool jit_ok = J && (pht::jit_what(J) & need);
+    bool use_jit = false;
+    if (jit_ok) {
+        if (fam == PHT_KERNELS_SPECIALIZED) use_jit = true;
+        else if (fam == PHT_KERNELS_AUTO) use_jit = evalm || !warp_step;
+    }
+    if (use_jit) {
+        e = pht::jit_launch(J, mode, S, A, st);
         if (e != cudaSuccess) return cuda_fail(e);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return PHT_OK;
     }
-    // evaluation: the FP64 tensor-core kernel for n >= 11; up to n = 10 the warp-per-group kernel
-    // (k_stepw<N, EVAL_X>) is faster (cyclic-10 0.73 vs 0.62, noon-10 0.69 vs 0.61 G points/s;
-    // katsura-10, n = 11: 0.45 vs 0.58); PHT_DENSE=1 forces the tensor-core kernel
-    const char *fd = getenv("PHT_DENSE");
-    const bool dense = s->dense && evalm && (s->n >= 11 || (fd && fd[0] == '1') || mode == pht::MODE_EVAL_Z);
+    bool dense = false;
+    if (evalm && s->dense) {
+        if (fam == PHT_KERNELS_DENSE) dense = true;
+        else if (fam == PHT_KERNELS_AUTO || fam == PHT_KERNELS_SPECIALIZED)
+            dense = s->n >= 11 || mode == pht::MODE_EVAL_Z;
+    }
+    const int lfam = fam == PHT_KERNELS_TILE ? pht::FAM_TILE : pht::FAM_AUTO;
     const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff, s->max_ntk};
     switch (s->n) {
-#define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st); break;
+#define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st, lfam); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
         PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12) PHT_CASE(13) PHT_CASE(14)
         PHT_CASE(15) PHT_CASE(16) PHT_CASE(17) PHT_CASE(18) PHT_CASE(19) PHT_CASE(20) PHT_CASE(21)
@@ -604,12 +667,10 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
     if ((e = cudaEventRecord(s->hev0, st)) != cudaSuccess) return cuda_fail(e);
     for (int u = 0; u < PHT_HOST_STREAMS; ++u)
         if ((e = cudaStreamWaitEvent(s->hs[u], s->hev0, 0)) != cudaSuccess) return cuda_fail(e);
-    // chunks: 1/PHT_HOST_CHUNKS of the batch (default 32: measured 8 -> 416, 16 -> 453, 32 -> 471,
-    // 64 -> 453 M evals/s end to end on the bench step), at least 32K points (launch and copy
-    // latency stay amortised); the pipeline fill (first copy-in) and drain (last copy-out) are
-    // one chunk each
-    int nch = 32;
-    if (const char *ev = getenv("PHT_HOST_CHUNKS")) nch = std::max(1, atoi(ev));
+    // chunks: 1/32 of the batch (measured 8 -> 416, 16 -> 453, 32 -> 471, 64 -> 453 M evals/s end
+    // to end on the bench step), at least 32K points (launch and copy latency stay amortised); the
+    // pipeline fill (first copy-in) and drain (last copy-out) are one chunk each
+    const int nch = 32;
     int64_t chunk = (p + nch - 1) / nch;
     if (chunk < 32768) chunk = 32768;
     int c = 0;
@@ -722,7 +783,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     if (s->proj && (cellw || o.log_state)) return PHT_EUNSUPPORTED; // projective: y state only
     if (s->proj) o.pred_log = 0;
     if (!(o.dtau_init > 0) || !(o.dtau_min > 0) || !(o.dtau_max > 0) || !(o.shrink > 0 && o.shrink < 1) ||
-        !(o.grow >= 1) || o.newton_iters < 1 || o.grow_after < 1 || o.max_steps < 1 || o.final_iters < 0)
+        !(o.grow >= 1) || o.newton_iters < 1 || o.grow_after < 1 || o.max_steps < 1 || o.final_iters < 1)
         return PHT_EINVAL;
     DevGuard g(s->device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
@@ -747,18 +808,20 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
                          o.pred_log < 0 ? o.log_state : o.pred_log, o.pred_tol, o.predictor};
-    // the specialised tracker only with at least one full wave of paths: its tiles are 2-3x larger
-    // than the generic kernel's, so few paths would run on few SMs (measured: 70 paths 4x slower)
-    // (PHT_JIT_TRACK=1 forces it: tests)
-    const char *force = getenv("PHT_JIT_TRACK");
-    // the warp-per-group tracker (k_trackw: n <= 12, LU, affine, Euler predictor) is faster than
-    // the specialised tile tracker, which is used only where k_trackw does not apply
+    // AUTO: the warp-per-group tracker (k_trackw: n <= 12, LU, affine, Euler predictor) is faster
+    // than the specialised tile tracker, which serves only where k_trackw does not apply and the
+    // batch fills at least one wave of its (2-3x larger) tiles (measured: 70 paths 4x slower)
+    const int fam = s->kernels;
     const bool warp_track = s->n <= 12 && !s->proj && s->solver == PHT_SOLVER_LU && o.predictor != 1;
-    if (s->jit && (pht::jit_what(s->jit) & pht::JIT_TRACK) &&
-        ((!warp_track && p >= pht::jit_track_slots(s->jit, s->sms)) || (force && force[0] == '1')))
-        e = pht::jit_launch_track(s->jit, S, A, st, s->sms);
+    pht::JitKernels *J = jit_snapshot(s);
+    const bool jit_ok = J && (pht::jit_what(J) & pht::JIT_TRACK);
+    const bool use_jit = jit_ok && (fam == PHT_KERNELS_SPECIALIZED ||
+                                    (fam == PHT_KERNELS_AUTO && !warp_track && p >= pht::jit_track_slots(J, s->sms)));
+    const int lfam = fam == PHT_KERNELS_TILE ? pht::FAM_TILE : pht::FAM_AUTO;
+    if (use_jit)
+        e = pht::jit_launch_track(J, S, A, st, s->sms);
     else switch (s->n) {
-#define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms); break;
+#define PHT_CASE(N) case N: e = pht::launch_track<N>(S, A, st, s->sms, lfam); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
         PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12) PHT_CASE(13) PHT_CASE(14)
         PHT_CASE(15) PHT_CASE(16) PHT_CASE(17) PHT_CASE(18) PHT_CASE(19) PHT_CASE(20) PHT_CASE(21)
@@ -808,4 +871,4 @@ extern "C" const char *pht_strerror(int code)
     }
 }
 
-extern "C" int pht_version(void) { return 1; }
+extern "C" int pht_version(void) { return 2; }

@@ -241,13 +241,15 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
                     el[m] = ed[m] * KC[13];
                 } else if ((mx - eh[m]) - el[m] > 512.0) { // exact power-of-two rescale
                     const double e2 = rint(mx * KC[14]);
-                    const double f = scalbn(1.0, (int)fmax(ed[m] - e2, -2000.0));
+                    // two normal factors (see RowAcc::reduce): one 2^d underflows for d < -1074
+                    const int d = (int)fmax(ed[m] - e2, -2000.0), d1 = d / 2;
+                    const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d - d1);
 #pragma unroll
                     for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
-                            acc[m][ct][u][0] *= f;
-                            acc[m][ct][u][1] *= f;
+                            acc[m][ct][u][0] = acc[m][ct][u][0] * f1 * f2;
+                            acc[m][ct][u][1] = acc[m][ct][u][1] * f1 * f2;
                         }
                     ed[m] = e2;
                     eh[m] = e2 * KC[12];

@@ -43,7 +43,11 @@ namespace pht {
 
 enum Mode : int { MODE_EVAL_X = 0, MODE_EVAL_Z = 1, MODE_DIRS = 2, MODE_STEP = 3 };
 
-enum : int { PT_ZERO_COORD = 1, PT_NONFINITE = 2, PT_SINGULAR = 4 };
+enum : int { PT_ZERO_COORD = 1, PT_NONFINITE = 2, PT_SINGULAR = 4, PT_FLOOR = 64 };
+
+// Kernel families (include/pht.h pht_system_set_kernels): AUTO = the measured-best family per
+// entry point; the others force one family wherever it implements the entry point.
+enum : int { FAM_AUTO = 0, FAM_TILE = 1, FAM_WARP = 2, FAM_DENSE = 3, FAM_SPECIALIZED = 4 };
 
 enum : int { SOLVER_LU = 0, SOLVER_QR = 1 };
 
@@ -512,11 +516,15 @@ struct RowAcc {
         double y = reduced(phi);
         if (__builtin_expect(y > 512.0, 0)) { // rare: rescale everything to the new leading term (exact power of two)
             const double e2 = rint(phi * KC[14]);
-            const double f = scalbn(1.0, (int)fmax(ed - e2, -2000.0));
+            // the shift d = ed - e2 lies in [-2000, -738]: applied as two factors 2^d1 2^d2 (each >=
+            // 2^-1000, normal), because the accumulators hold up to ~2^745 and a single 2^d would
+            // underflow to 0 for d < -1074 although the rescaled entries are representable
+            const int d = (int)fmax(ed - e2, -2000.0), d1 = d / 2, d2 = d - d1;
+            const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d2);
 #pragma unroll
-            for (int j = 0; j < N; ++j) g[j] = make_double2(g[j].x * f, g[j].y * f);
-            gt = make_double2(gt.x * f, gt.y * f);
-            h = make_double2(h.x * f, h.y * f);
+            for (int j = 0; j < N; ++j) g[j] = make_double2(g[j].x * f1 * f2, g[j].y * f1 * f2);
+            gt = make_double2(gt.x * f1 * f2, gt.y * f1 * f2);
+            h = make_double2(h.x * f1 * f2, h.y * f1 * f2);
             set_exp(e2);
             y = reduced(phi);
         }
@@ -1178,6 +1186,12 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
 
 
 // ---------------------------------------------------------------------------------------
+#ifndef PHT_STEPW_PAIR
+#define PHT_STEPW_PAIR(n) PHT_PAIR(n) // two terms per iteration in k_stepw's row loop
+#endif
+#ifndef PHT_STEPW_RTREG
+#define PHT_STEPW_RTREG 0 // experiments: (rho, vartheta) in registers in k_stepw's row loop
+#endif
 // Warp-per-group Euler-Newton step (pht_pc_step, LU, affine).  One warp owns a
 // group of PPW = 32/N points and keeps ONE lane mapping through every stage: lane (q, i) = (point
 // q of the group, index i).  It loads x_i, runs stage 1 for variable i, evaluates ROW i of the
@@ -1246,9 +1260,14 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
                                            int k, int q, double2 (&row)[N + 2], int &e)
 {
     constexpr int RS = rec_stride(N), PPW = GeoW<N>::PPW;
+#if PHT_STEPW_RTREG
+    PointLog<N, false> pl; // (rho, vartheta) of the point in registers for the whole row
+    pl.template load<PPW>(W.rt, q);
+#else
     PointLog<N, true> pl;
     pl.base = &W.rt[0][q];
     pl.stride = PPW;
+#endif
     const double tau = W.tau[q];
     const int m = sm.mk[k];
     const double2 *rec = R + (size_t)k * (RS / 2);
@@ -1260,7 +1279,7 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
         acc.init(phi_of<N>(a, pl, tau));
     }
     int i = 0;
-    for (; PHT_PAIR(N) && i + 1 < m; i += 2) {
+    for (; PHT_STEPW_PAIR(N) && i + 1 < m; i += 2) {
         double a[RS], b[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
         load_rec_s<N>(rec + (size_t)(i + 1) * TS, b);
@@ -1713,8 +1732,10 @@ __device__ __forceinline__ void trk_decide(TT &T, const TrackArgs &A, const DevS
             const bool finite = S.proj ? (sqrt(fma(yn.x, yn.x, yn.y * yn.y)) * o.inf_norm >= 1.0)
                                        : (LOGS ? (xinf <= log(o.inf_norm)) : (xinf <= o.inf_norm));
             if (sqrt(nd) <= o.final_tol) finish = finite ? 0 : 32;
-            else if (T.fin[qq] >= o.final_iters) // accuracy floor: accept at newton_tol (R14)
-                finish = (sqrt(nd) <= o.newton_tol && finite) ? 0 : 32;
+            else if (T.fin[qq] >= o.final_iters) // not refined to final_tol (ledger A24): DIVERGED,
+                // or FLOOR when the corrections reached newton_tol -- a finite endpoint at the log/exp
+                // evaluation's accuracy floor (reading R30), reported apart from OK
+                finish = (sqrt(nd) <= o.newton_tol && finite) ? PT_FLOOR : 32;
         }
     }
     if (reject) {
@@ -1877,6 +1898,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             // flush the last finished paths
             if (tid < N * PTS) {
                 const int qq = tid / N, j = tid % N;
+                if (T.acc[qq]) T.xa[j][qq] = T.xt[j][qq]; // accepted in the last iteration (MAX_STEPS)
                 if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
             }
             break;
@@ -2082,6 +2104,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
         __syncwarp();
         const bool busy = __any_sync(0xffffffffu, lane < PPW && W.phase[lane] != PH_IDLE);
         if (!busy) {
+            if (inseg && W.acc[q]) W.xa[i][q] = W.xt[i][q]; // accepted in the last iteration (MAX_STEPS)
             if (inseg && W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
             break;
         }
@@ -2093,9 +2116,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
 template <int N>
 bool trackw_eligible(const DevSys &S, const TrackArgs &A)
 {
-    if (N > 12 || S.proj || A.solver != SOLVER_LU || A.o.predictor == 1 || S.mt <= 0) return false;
-    const char *ev = getenv("PHT_TRACKW");
-    return !(ev && ev[0] == '0');
+    return N <= 12 && !S.proj && A.solver == SOLVER_LU && A.o.predictor != 1 && S.mt > 0;
 }
 
 template <int N, bool LOGS>
@@ -2147,10 +2168,11 @@ cudaError_t launch_track_t(const DevSys &S, const TrackArgs &A, cudaStream_t str
     return cudaGetLastError();
 }
 
+// family: FAM_TILE forces k_track; otherwise k_trackw where eligible (FAM_AUTO, FAM_WARP)
 template <int N>
-cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+cudaError_t launch_track(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms, int family)
 {
-    if (trackw_eligible<N>(S, A)) {
+    if (family != FAM_TILE && trackw_eligible<N>(S, A)) {
         const cudaError_t e = A.o.log_state ? launch_trackw_t<N, true>(S, A, stream, sms)
                                             : launch_trackw_t<N, false>(S, A, stream, sms);
         if (e != cudaErrorNotSupported) return e;
@@ -2221,18 +2243,14 @@ cudaError_t launch_eval_mode(const DevSys &S, const Args &A, cudaStream_t stream
 template <int N>
 bool stepw_eligible(const DevSys &S, const Args &A)
 {
-    if (N > 12 || S.proj || A.solver != SOLVER_LU || S.mt <= 0) return false;
-    const char *ev = getenv("PHT_STEPW");
-    return !(ev && ev[0] == '0');
+    return N <= 12 && !S.proj && A.solver == SOLVER_LU && S.mt > 0;
 }
 
 // pht_evaluate through k_stepw<N, EVAL_X>: affine systems, n <= 12 (cyclic-5 2.44 -> 3.24, cyclic-10
-// 0.59 -> 0.73 G points/s over the tile kernel k_phte); PHT_EVALW=0 selects k_phte
+// 0.59 -> 0.73 G points/s over the tile kernel k_phte)
 template <int N>
 bool stepw_eval_eligible(const DevSys &S)
 {
-    const char *ev = getenv("PHT_EVALW");
-    if (ev && ev[0] == '0') return false;
     return N <= 12 && !S.proj && S.mt > 0;
 }
 
@@ -2264,25 +2282,27 @@ cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
     return cudaGetLastError();
 }
 
-// Host-side launcher for one n (instantiated per n in inst_n*.cu).
+// Host-side launcher for one n (instantiated per n in inst_n*.cu).  family: FAM_TILE forces the
+// tile kernels (k_phte, k_pht); otherwise the warp-per-group kernel k_stepw where eligible.
 template <int N>
-cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream)
+cudaError_t launch(int mode, const DevSys &S, const Args &A, cudaStream_t stream, int family)
 {
+    const bool tile = family == FAM_TILE;
     switch (mode) {
     case MODE_EVAL_X: {
         cudaError_t e = cudaErrorNotSupported;
-        if (stepw_eval_eligible<N>(S)) e = launch_stepw<N, MODE_EVAL_X>(S, A, stream);
+        if (!tile && stepw_eval_eligible<N>(S)) e = launch_stepw<N, MODE_EVAL_X>(S, A, stream);
         return e == cudaErrorNotSupported ? launch_eval_mode<N, MODE_EVAL_X>(S, A, stream) : e;
     }
     case MODE_EVAL_Z: return launch_eval_mode<N, MODE_EVAL_Z>(S, A, stream);
     case MODE_DIRS: {
         cudaError_t e = cudaErrorNotSupported;
-        if (stepw_eligible<N>(S, A)) e = launch_stepw<N, MODE_DIRS>(S, A, stream);
+        if (!tile && stepw_eligible<N>(S, A)) e = launch_stepw<N, MODE_DIRS>(S, A, stream);
         return e == cudaErrorNotSupported ? launch_mode<N, MODE_DIRS>(S, A, stream) : e;
     }
     case MODE_STEP: {
         cudaError_t e = cudaErrorNotSupported;
-        if (stepw_eligible<N>(S, A)) e = launch_stepw<N, MODE_STEP>(S, A, stream);
+        if (!tile && stepw_eligible<N>(S, A)) e = launch_stepw<N, MODE_STEP>(S, A, stream);
         return e == cudaErrorNotSupported ? launch_mode<N, MODE_STEP>(S, A, stream) : e;
     }
     default: return cudaErrorInvalidValue;

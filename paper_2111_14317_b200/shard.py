@@ -8,9 +8,11 @@ endpoints, statuses and statistics on rank 0.
 * `shard_indices`: a seeded permutation of the path indices (so paths of the same mixed cell,
   which have similar lengths, spread over the ranks), cut into `world` contiguous blocks whose
   sizes differ by at most one.
-* `gather_to_rank0`: pads each rank's block to the common size, one `all_gather_into_tensor` per
-  result tensor (NCCL over NVLink on GPUs, gloo on CPU), and rank 0 restores the original path
-  order.  Works with CPU tensors (gloo) and CUDA tensors (nccl) alike.
+* `gather_to_rank0`: packs every per-path result of this rank (path index, endpoint re/im,
+  status, statistics) into ONE float64 row per path, pads the block to the common size and runs
+  exactly ONE `all_gather_into_tensor` (NCCL over NVLink on GPUs, gloo on CPU); rank 0 unpacks
+  and restores the original path order.  Integers travel as float64 (exact below 2^53).
+  Works with CPU tensors (gloo) and CUDA tensors (nccl) alike.
 """
 from __future__ import annotations
 
@@ -34,43 +36,62 @@ def block_size(n_paths: int, world: int) -> int:
     return -(-n_paths // world)
 
 
-def gather_to_rank0(local: dict, indices: np.ndarray, n_paths: int, group=None) -> dict | None:
-    """Gather per-path result tensors (first dim = this rank's paths, in `indices` order) to rank 0.
+def _columns(t: torch.Tensor) -> int:
+    """float64 columns one path's entry of t occupies in the packed row."""
+    per = 1
+    for d in t.shape[1:]:
+        per *= int(d)
+    return per * (2 if t.is_complex() else 1)
 
-    Returns on rank 0 a dict of tensors with first dim n_paths in the original path order,
-    None elsewhere.  One all_gather per tensor; the padding rows carry index -1.
+
+def gather_to_rank0(local: dict, indices: np.ndarray, n_paths: int, group=None) -> dict | None:
+    """Gather per-path result tensors (first dim = this rank's paths, in `indices` order) to rank 0
+    with ONE collective (minimise communication between devices).
+
+    Row layout (float64): [path index | each tensor's entries, complex as (re, im) pairs, integers
+    converted exactly].  Returns on rank 0 a dict of tensors with first dim n_paths in the
+    original path order and the original dtypes; None elsewhere.  Padding rows carry index -1.
     """
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     B = block_size(n_paths, world)
     any_t = next(iter(local.values()))
     dev = any_t.device
-    idx = torch.full((B,), -1, dtype=torch.int64, device=dev)
-    idx[:len(indices)] = torch.as_tensor(indices, dtype=torch.int64, device=dev)
-    all_idx = torch.empty((world * B,), dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(all_idx, idx, group=group)
-    out = {}
-    for name, t in local.items():
-        if t.shape[0] != len(indices):
-            raise ValueError(f"{name}: first dim {t.shape[0]} != {len(indices)} local paths")
-        pad = torch.zeros((B,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-        pad[:t.shape[0]] = t
-        if t.is_complex():  # gloo/nccl all_gather on complex: go through a real view
-            pad_r = torch.view_as_real(pad).contiguous()
-            buf = torch.empty((world * B,) + tuple(pad_r.shape[1:]), dtype=pad_r.dtype, device=dev)
-            dist.all_gather_into_tensor(buf, pad_r, group=group)
-            buf = torch.view_as_complex(buf)
-        else:
-            buf = torch.empty((world * B,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-            dist.all_gather_into_tensor(buf, pad.contiguous(), group=group)
-        out[name] = buf
+    names = list(local)
+    cols = [_columns(local[k]) for k in names]
+    width = 1 + sum(cols)
+    row = torch.zeros((B, width), dtype=torch.float64, device=dev)
+    row[:, 0] = -1.0
+    m = len(indices)
+    row[:m, 0] = torch.as_tensor(indices, dtype=torch.float64, device=dev)
+    c = 1
+    for k, w in zip(names, cols):
+        t = local[k]
+        if t.shape[0] != m:
+            raise ValueError(f"{k}: first dim {t.shape[0]} != {m} local paths")
+        # (integer results -- statuses, step counts -- are far below 2^53; not checked on the device,
+        # which would synchronise inside the caller's timed region)
+        v = torch.view_as_real(t.contiguous()) if t.is_complex() else t
+        row[:m, c:c + w] = v.reshape(m, w).to(torch.float64)
+        c += w
+    buf = torch.empty((world * B, width), dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(buf, row, group=group)          # the one collective
     if rank != 0:
         return None
-    keep = all_idx >= 0
-    order = all_idx[keep]
+    keep = buf[:, 0] >= 0
+    order = buf[keep, 0].to(torch.int64)
+    data = buf[keep]
     res = {}
-    for name, buf in out.items():
-        full = torch.empty((n_paths,) + tuple(buf.shape[1:]), dtype=buf.dtype, device=dev)
-        full[order] = buf[keep]
-        res[name] = full
+    c = 1
+    for k, w in zip(names, cols):
+        t = local[k]
+        part = data[:, c:c + w]
+        c += w
+        full = torch.empty((n_paths, w), dtype=torch.float64, device=dev)
+        full[order] = part
+        if t.is_complex():
+            out = torch.view_as_complex(full.reshape((n_paths,) + tuple(t.shape[1:]) + (2,)).contiguous())
+            res[k] = out.to(t.dtype)
+        else:
+            res[k] = full.reshape((n_paths,) + tuple(t.shape[1:])).to(t.dtype)
     return res

@@ -32,7 +32,7 @@ def test_binding_covers_header():
 def test_version_and_strerror_without_gpu():
     from paper_2111_14317_b200 import _lib
     lib = _lib.load()
-    assert lib.pht_version() == 1
+    assert lib.pht_version() == 2
     assert lib.pht_strerror(-3).decode().startswith("duplicate")
     assert lib.pht_launch_count() >= 0
 
@@ -98,3 +98,39 @@ def test_packer_terms_are_monomial_lifting_pairs():
     c = np.ones(2, np.complex128)
     assert lib.pht_specialize_source(1, 1, P(off), P(ex), P(c), P(np.array([0.0, 1.0])), None, 0) > 0
     assert lib.pht_specialize_source(1, 1, P(off), P(ex), P(c), P(np.array([1.0, 1.0])), None, 0) == -3
+
+
+def test_set_kernels_validates_without_gpu():
+    from paper_2111_14317_b200 import _lib
+    lib = _lib.load()
+    assert lib.pht_system_set_kernels(None, _lib.KERNELS["auto"]) == -1   # NULL handle
+    assert lib.pht_system_kernels(None) == -1
+
+
+def test_pc_step_host_rejects_bad_host_buffers():
+    """ADVICE r1: pht_pc_step_host reads/writes p*n*16 bytes of x and p*8 of tau/dtau/dn_norm;
+    the binding refuses wrong dtype, shape, stride or read-only buffers before any C call."""
+    import numpy as np
+    import paper_2111_14317_b200 as P
+    g = P.System.__new__(P.System)          # validation runs before the handle is touched
+    g.n = 4
+    p = 8
+    x = np.ones((p, 4), np.complex128)
+    tau = np.zeros(p)
+    dtau = np.full(p, 0.01)
+    bad = [
+        (x.astype(np.complex64), tau, dtau, {}),
+        (np.ones((p, 3), np.complex128), tau, dtau, {}),
+        (np.ones((p, 8), np.complex128)[:, ::2], tau, dtau, {}),
+        (x, tau[:-1], dtau, {}),
+        (x, tau, dtau.astype(np.float32), {}),
+        (x, tau, dtau, {"status": np.zeros(p, np.int32)}),
+        (x, tau, dtau, {"dn_norm": np.zeros(p - 1)}),
+    ]
+    for xx, tt, dd, kw in bad:
+        with pytest.raises(P.PhtError):
+            g.pc_step_host(xx, tt, dd, 1, **kw)
+    ro = x.copy()
+    ro.flags.writeable = False
+    with pytest.raises(P.PhtError):
+        g.pc_step_host(ro, tau, dtau, 1)

@@ -126,10 +126,9 @@ def _stage1_oracle(G):
 
 
 @pytest.mark.parametrize("spec", [False, True])
-def test_proj_track_solution_at_infinity(P, spec, monkeypatch):
+def test_proj_track_solution_at_infinity(P, spec):
     """Second stage to F = {x1 + x2 - 1, x1^2 + x1 x2 + x1 + x2 - 3}: one finite solution (2, -1),
     one at the point at infinity (1 : -1 : 0); same statuses and endpoints as the oracle."""
-    monkeypatch.setenv("PHT_JIT_TRACK", "1")
     eqs = [[((1, 0), 1.0), ((0, 1), 1.0), ((0, 0), -1.0)],
            [((2, 0), 1.0), ((1, 1), 1.0), ((1, 0), 1.0), ((0, 1), 1.0), ((0, 0), -3.0)]]
     F = W.from_terms("inf2", 2, eqs, coeffs="native", lift_max=100)
@@ -139,7 +138,7 @@ def test_proj_track_solution_at_infinity(P, spec, monkeypatch):
     yo, _, so, _ = oracle.Oracle(H2).proj_track(y1, np.full(2, PH.TAU0))
     g = P.System.from_workload(H2, projective=True)
     if spec:
-        g.specialize()
+        g.specialize().set_kernels("specialized")  # also the tracker on 2 paths
     yd, td = _cuda(y1), _cuda(np.full(2, PH.TAU0))
     st, _ = g.track(yd, td)
     yg, sg = yd.cpu().numpy(), st.cpu().numpy()

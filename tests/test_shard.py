@@ -38,11 +38,20 @@ def _worker(rank, world, port, n, q):
     x = torch.tensor([[complex(i, -i), complex(2 * i, 1)] for i in idx], dtype=torch.complex128).reshape(-1, 2)
     st = torch.tensor([i % 7 for i in idx], dtype=torch.uint8)
     stats = torch.tensor([[i, 2 * i, 3 * i, 4] for i in idx], dtype=torch.int64).reshape(-1, 4)
-    out = gather_to_rank0({"x": x, "status": st, "stats": stats}, idx, n)
+    calls = []
+    orig = dist.all_gather_into_tensor
+    dist.all_gather_into_tensor = lambda *a, **k: (calls.append(1), orig(*a, **k))[1]
+    try:
+        out = gather_to_rank0({"x": x, "status": st, "stats": stats}, idx, n)
+    finally:
+        dist.all_gather_into_tensor = orig
+    assert len(calls) == 1          # exactly one collective
     if rank == 0:
         ok = (torch.equal(out["x"][:, 0].real, torch.arange(n, dtype=torch.float64))
               and torch.equal(out["status"], torch.tensor([i % 7 for i in range(n)], dtype=torch.uint8))
-              and torch.equal(out["stats"][:, 1], 2 * torch.arange(n)))
+              and torch.equal(out["stats"][:, 1], 2 * torch.arange(n))
+              and out["x"].dtype == torch.complex128 and out["status"].dtype == torch.uint8
+              and torch.equal(out["x"][:, 1].imag, torch.ones(n, dtype=torch.float64)))
         q.put(bool(ok))
     else:
         assert out is None

@@ -9,4 +9,4 @@ from .systems import (  # noqa: F401
     System, cyclic, katsura, noon, chandra, random_dense, diagonal, from_terms,
     MASTER_SEED,
 )
-from .points import random_points, random_log_points  # noqa: F401
+from .points import random_points, random_log_points, random_extended_points  # noqa: F401
