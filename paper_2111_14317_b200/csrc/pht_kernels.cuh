@@ -277,7 +277,9 @@ __device__ __forceinline__ void log_split(double2 x, double &rho, double &th, do
 // Table-driven: 2^(j/256) and cis(2 pi j/256) in shared memory, degree-4/5/6 polynomials on
 // the reduced arguments (|r| <= ln2/512, |s| <= pi/256); error <= ~4 ulp.
 // PHT_TAB64=1: 64-entry bank-replicated tables, degree 5/7/8 (|r| <= ln2/128, |s| <= pi/64).
-__device__ __forceinline__ double2 expcis(double y, double th, const double *etab, const double2 *ctab)
+template <bool TL = false>
+__device__ __forceinline__ double2 expcis(double y, double th, const double *etab, const double2 *ctab,
+                                          double th_lo = 0.0)
 {
     // terms more than e^-2000 below the row scale flush to 0; clamping first keeps y*256/ln2
     // inside the 32-bit integer extracted from the shifter (|y| up to ~10^8 occurs for large
@@ -320,12 +322,13 @@ __device__ __forceinline__ double2 expcis(double y, double th, const double *eta
     const unsigned hi = (unsigned)__double2hiint(mag) + ((unsigned)m << 20);
     mag = (m < -1000) ? 0.0 : __hiloint2double((int)hi, __double2loint(mag));
 
-    const double qf = fma(th, KC[5], SHIFT);
+    const double qf = fma(TL ? th + th_lo : th, KC[5], SHIFT);
     const int qi = __double2loint(qf);
     const double qd = qf - SHIFT;
-    double s = fma(qd, -KC[6], th);
+    double s = fma(qd, -KC[6], th); // exact for the compensated th (TL): th is a multiple of 2^-20
     s = fma(qd, -KC[7], s);
     s = fma(qd, -KC[8], s);
+    if (TL) s += th_lo;
     const double s2 = s * s;
     const double sn = fma(s * s2, fma(s2, KC[9], KC[10]), s);
     const double cs = fma(s2, fma(s2, fma(s2, KC[11], KC[3]), -0.5), 1.0);
@@ -342,6 +345,11 @@ __device__ __forceinline__ double2 expcis(double y, double th, const double *eta
 #ifndef PHT_PAIR
 #define PHT_PAIR(n) ((n) <= 8)
 #endif
+#ifndef PHT_STEPW_UNROLL
+#define PHT_STEPW_UNROLL 1 // unroll factor of k_stepw's single-term row loop (experiments)
+#endif
+constexpr int kStepwUnroll = PHT_STEPW_UNROLL; // (#pragma unroll does not expand macros)
+
 
 // ---- tile geometry --------------------------------------------------------------------
 // W layout (evaluation): WL point lanes per equation, thread (k, q) = (tid / WL, tid % WL).
@@ -495,6 +503,36 @@ __device__ __forceinline__ double phi_of(const double (&a)[rec_stride(N)], const
     return p0 + p1;
 }
 
+// Compensated stage 2 for the tracker's final refinement (reading R30): each log
+// coordinate is split exactly as v = v_hi + v_lo with v_hi a multiple of 2^-20 (|v| < 2^30), so
+// sum_j a_j v_hi_j is exact (|a_j| <= 1024) and the rounding of the dot product moves to the small
+// part: phi = phi_hi + phi_lo, theta = th_hi + th_lo with an absolute error ~u instead of u |phi|.
+__device__ __forceinline__ double split_hi(double v)
+{
+    const double C = 0x1.8p+32; // 1.5 * 2^32: rounds |v| < 2^30 to a multiple of 2^-20
+    const double h = (v + C) - C;
+    return (fabs(v) < 0x1p30) ? h : v;
+}
+template <int N, class PL>
+__device__ __forceinline__ void phi_theta_c(const double (&a)[rec_stride(N)], const PL &pl, double tau, double &ph,
+                                            double &pl_, double &th, double &tl)
+{
+    double p0 = 0.0, p1 = fma(a[N], tau, a[N + 1]), t0 = 0.0, t1 = a[N + 2];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double2 v = pl.get(j);
+        const double rh = split_hi(v.x), vh = split_hi(v.y);
+        p0 = fma(a[j], rh, p0);          // exact
+        p1 = fma(a[j], v.x - rh, p1);    // v.x - rh exact
+        t0 = fma(a[j], vh, t0);
+        t1 = fma(a[j], v.y - vh, t1);
+    }
+    ph = p0;
+    pl_ = p1;
+    th = t0;
+    tl = t1;
+}
+
 // Row accumulator with an online binary row exponent e (ledger R7): the row holds
 // sum_i w_i 2^-e; a term more than e^512 above the current scale rescales the row exactly.
 template <int N>
@@ -511,6 +549,11 @@ struct RowAcc {
     }
     __device__ __forceinline__ void set_exp(double e) { ed = e; }
     __device__ __forceinline__ double reduced(double phi) const { return fma(-ed, KC[13], fma(-ed, KC[12], phi)); }
+    // the same for phi = ph + pl (compensated stage 2): ph - e LN2_HI is exact
+    __device__ __forceinline__ double reduced2(double ph, double pl) const
+    {
+        return fma(-ed, KC[12], ph) + fma(-ed, KC[13], pl);
+    }
     __device__ __forceinline__ double reduce(double phi)
     {
         double y = reduced(phi);
@@ -559,7 +602,7 @@ __device__ void jit_row(const DevSys &S, const Smem<N> &sm, int k, int q, double
 // Terms are processed two at a time (independent dependency chains for the FP64 pipe).
 // wq (optional): per-point lifting table (cell-shifted liftings omega', pht_track_cells); the
 // term's omega is replaced by wq[i] (global term index i).
-template <int N>
+template <int N, bool COMP = false>
 __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int k, int q,
                                          double2 (&row)[N + 2], int &e, const double *wq = nullptr)
 {
@@ -594,6 +637,17 @@ __device__ __forceinline__ void eval_row(const DevSys &S, const Smem<N> &sm, int
         acc.init(phi_of<N>(a, pl, tau));
     }
     int i = 0;
+    if (COMP) { // compensated stage 2 for the tracker's final refinement (reading R30)
+        for (; i < m; ++i) {
+            double a[RS];
+            load_rec<N>(rec + (size_t)i * (RS / 2), a);
+            if (wk) a[N] = __ldg(wk + i);
+            double ph, pl_, th, tl;
+            phi_theta_c<N>(a, pl, tau, ph, pl_, th, tl);
+            acc.reduce(ph + pl_);
+            acc.add(a, expcis<true>(acc.reduced2(ph, pl_), th, sm.exptab, sm.cistab, tl));
+        }
+    }
     // two terms per iteration only while the register budget allows it (ILP vs spills)
     for (; PHT_PAIR(N) && i + 1 < m; i += 2) {
         double a[RS], b[RS];
@@ -700,9 +754,22 @@ __device__ __forceinline__ void store_row(Smem<N> &sm, int k, int q, double2 (&r
 // G [dE | dN] = -[G_tau | h].
 // The elimination on rows held in registers: lane (seg0 = lane / N, i) holds row i of its point;
 // prow: the point's pivot-row buffer (N + 2 entries, shared memory), kseg: its pivot keys (PPW > 4).
-template <int N, int PPW, int KS>
+// Pivot-row broadcast: PHT_W_SHFL = 1 moves the pivot row lane-to-lane with shuffles (4 SHFL per
+// complex entry, no shared-memory store/load and no __syncwarp per pivot); 0 publishes it through
+// the point's shared buffer prow.  IMAJ: lane order of the caller, index-major (lane = i * PPW +
+// seg, warp-per-group kernels) or point-major (lane = seg * N + i, tile kernels).
+#ifndef PHT_W_SHFL
+#define PHT_W_SHFL 0
+#endif
+__device__ __forceinline__ double2 shfl2(double2 v, int src)
+{
+    return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+template <int N, int PPW, int KS, bool IMAJ = false, int LPR = 1>
 __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, unsigned *kseg, int seg0, int seg,
-                                            int i, bool act, int &col, double2 &dE, double2 &dN, bool &singular)
+                                            int i, bool act, int &col, double2 &dE, double2 &dN, bool &singular,
+                                            bool prim = true)
 {
     constexpr int RW = N + 2;
     unsigned long long rbits = 0ull;
@@ -732,7 +799,7 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
                 kmax = (seg == sg) ? m : kmax;
             }
         } else {
-            if (act) kseg[i] = key;
+            if (act && prim) kseg[i] = key;
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < KS; u += 4) {
@@ -749,7 +816,22 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
             used = true;
             col = j;
         }
-        if (me && act) {
+#if PHT_W_SHFL
+        const int src = IMAJ ? (r * PPW + seg) * LPR : seg * N + r; // a lane holding this point's pivot row
+        const double2 rcp = shfl2(crcp, src);
+        {
+            const double pa = cabs1(a[j]);
+            singular = singular || (me && !(pa > thr && pa < 0x1p510));
+            myrcp = me ? crcp : myrcp;
+        }
+        double2 l = cmul(a[j], rcp);
+        l = me ? make_double2(0.0, 0.0) : l;
+#pragma unroll
+        for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, shfl2(a[c], src));
+        a[j] = me ? a[j] : make_double2(0.0, 0.0);
+        if (PPW > 4) __syncwarp(); // kseg is rewritten by the next pivot search
+#else
+        if (me && act && prim) {
             // the pivot row with the pivot replaced by its reciprocal (computed before the
             // argmax by every lane for its own candidate: the reciprocal's latency overlaps the
             // pivot search instead of following the row broadcast)
@@ -765,13 +847,16 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
             singular = singular || (me && !(pa > thr && pa < 0x1p510));
             myrcp = me ? crcp : myrcp;
         }
-        // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row
+        // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row (measured:
+        // predicating the elimination on !me and re-reading the pivot reciprocal from prow at the
+        // end, which saves ~80 selects, is 2% slower -- the divergent branch costs more)
         double2 l = cmul(a[j], rcp);
         l = me ? make_double2(0.0, 0.0) : l;
 #pragma unroll
         for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, prow[c]);
         a[j] = me ? a[j] : make_double2(0.0, 0.0);
         __syncwarp();
+#endif
     }
     const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
     dE = make_double2(-e.x, -e.y);
@@ -1243,14 +1328,64 @@ struct SmemW {
     // followed by the records R[MT][N][rec_stride(N) / 2] (double2)
 };
 
+// Term records of the warp-per-group kernels in shared memory.  PHT_W_REC16 = 1: compact records
+// of 3 x 16 B per term (n <= 12): the exponents as int16 (exact: |a| <= PHT_MAX_EXP = 1024) in the
+// first 24 bytes, then omega, log|c|, arg c as doubles; a term costs 3 LDS.128 instead of
+// rec_stride(n) / 2 (7 at n = 10) and each exponent one I2F.F64.S16.  0: the packer's double records.
+// Measured (cyclic-10 step, ncu): shared-memory wavefronts -18%, time -0.6% (the step kernel is
+// latency-bound at 16 warps per SM, not shared-pipe-bound); noon-10 tracking 34.4 -> 32.7 ms.
+#ifndef PHT_W_REC16
+#define PHT_W_REC16 1
+#endif
+template <int N>
+struct RecW {
+    static constexpr bool C16 = PHT_W_REC16 && N <= 12;     // compact layout (the kernels run for n <= 12)
+    static constexpr int U = C16 ? 3 : rec_stride(N) / 2;  // 16-byte units per term
+};
+
+// one record, packer layout (rec_stride(N) doubles from global memory) -> shared-memory layout
+template <int N>
+__device__ __forceinline__ void pack_rec_w(const double2 *src, double2 *dst)
+{
+    if (RecW<N>::C16) {
+        unsigned e[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+        for (int j = 0; j < N && j < 12; ++j) {
+            const double2 v = __ldg(src + j / 2);
+            const int a = (int)((j & 1) ? v.y : v.x);
+            e[j >> 1] |= ((unsigned)a & 0xffffu) << (16 * (j & 1));
+        }
+        const double w = ((N & 1) ? __ldg(src + N / 2).y : __ldg(src + N / 2).x);
+        const double lc = ((N + 1) & 1) ? __ldg(src + (N + 1) / 2).y : __ldg(src + (N + 1) / 2).x;
+        const double ac = ((N + 2) & 1) ? __ldg(src + (N + 2) / 2).y : __ldg(src + (N + 2) / 2).x;
+        uint4 *d = reinterpret_cast<uint4 *>(dst);
+        d[0] = make_uint4(e[0], e[1], e[2], e[3]);
+        d[1] = make_uint4(e[4], e[5], (unsigned)__double2loint(w), (unsigned)__double2hiint(w));
+        d[2] = make_uint4((unsigned)__double2loint(lc), (unsigned)__double2hiint(lc), (unsigned)__double2loint(ac),
+                          (unsigned)__double2hiint(ac));
+    } else {
+        for (int u = 0; u < rec_stride(N) / 2; ++u) dst[u] = __ldg(src + u);
+    }
+}
+
 template <int N>
 __device__ __forceinline__ void load_rec_s(const double2 *r, double (&a)[rec_stride(N)])
 {
+    if (RecW<N>::C16) {
+        const uint4 *u = reinterpret_cast<const uint4 *>(r);
+        const uint4 u0 = u[0], u1 = u[1], u2 = u[2];
+        const unsigned e[6] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y};
 #pragma unroll
-    for (int u = 0; u < rec_stride(N) / 2; ++u) {
-        const double2 v = r[u];
-        a[2 * u] = v.x;
-        a[2 * u + 1] = v.y;
+        for (int j = 0; j < N && j < 12; ++j) a[j] = (double)(short)(e[j >> 1] >> (16 * (j & 1))); // I2F.F64.S16
+        a[N] = __hiloint2double((int)u1.w, (int)u1.z);
+        a[N + 1] = __hiloint2double((int)u2.y, (int)u2.x);
+        a[N + 2] = __hiloint2double((int)u2.w, (int)u2.z);
+    } else {
+#pragma unroll
+        for (int u = 0; u < rec_stride(N) / 2; ++u) {
+            const double2 v = r[u];
+            a[2 * u] = v.x;
+            a[2 * u + 1] = v.y;
+        }
     }
 }
 
@@ -1270,8 +1405,8 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
 #endif
     const double tau = W.tau[q];
     const int m = sm.mk[k];
-    const double2 *rec = R + (size_t)k * (RS / 2);
-    constexpr size_t TS = (size_t)N * (RS / 2); // record stride between terms of one equation
+    const double2 *rec = R + (size_t)k * RecW<N>::U;
+    constexpr size_t TS = (size_t)N * RecW<N>::U; // record stride between terms of one equation
     RowAcc<N> acc;
     {
         double a[RS];
@@ -1294,6 +1429,7 @@ __device__ __forceinline__ void eval_row_w(const SmemW<N> &sm, const double2 *R,
         acc.add(a, wa);
         acc.add(b, wb);
     }
+#pragma unroll kStepwUnroll
     for (; i < m; ++i) {
         double a[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
@@ -1324,10 +1460,10 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
     double2 *R = reinterpret_cast<double2 *>(smem_raw + ((sizeof(SmemW<N>) + 15) & ~(size_t)15));
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     load_tables(S, sm.exptab, sm.cistab, tid, G::SNT);
-    for (int idx = tid; idx < MT * N * (RS / 2); idx += G::SNT) { // records, term-major
-        const int u = idx % (RS / 2), kk = (idx / (RS / 2)) % N, t = idx / ((RS / 2) * N);
+    for (int idx = tid; idx < MT * N; idx += G::SNT) { // records, term-major (only t < m_k is read)
+        const int kk = idx % N, t = idx / N;
         const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
-        R[idx] = (t < m) ? __ldg(S.rec + (size_t)(i0 + t) * (RS / 2) + u) : make_double2(0.0, 0.0);
+        if (t < m) pack_rec_w<N>(S.rec + (size_t)(i0 + t) * (RS / 2), R + (size_t)idx * RecW<N>::U);
     }
     if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
     __syncthreads();
@@ -1405,7 +1541,7 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
             int col;
             double2 dE, dN;
             bool sing;
-            lsolve_regs<N, PPW, G::KS>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, act, col, dE, dN, sing);
+            lsolve_regs<N, PPW, G::KS, true>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, act, col, dE, dN, sing);
             if (act && DIRS) { // dx/dt = x (.) delta_E / t, dN_x = x (.) delta_N (Jx = G diag(1/x))
                 if (sing) atomicOr(&W.st[q], PT_SINGULAR);
                 const double2 xo = W.xs[col][q];
@@ -1813,12 +1949,19 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
         stage1<N, LOGS ? MODE_EVAL_Z : MODE_STEP>(sm, tid);
         if (tid < WL && tid >= PTS)
             for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
-        __syncthreads();
+        // any slot in the final refinement: the compensated stage 2 for the whole tile (R30)
+        const int comp = __syncthreads_or(tid < PTS && T.phase[tid] == PH_FINAL);
         if (k < N) {
             double2 row[N + 2];
             int e;
             const double *wq = A.cellw ? A.cellw + (size_t)T.cell[q] * A.M : nullptr;
-            eval_row<N>(S, sm, k, q, row, e, wq);
+#ifdef PHT_JIT
+            eval_row<N>(S, sm, k, q, row, e, wq); // generated rows: no compensated variant (FLOOR possible)
+            (void)comp;
+#else
+            if (comp) eval_row<N, true>(S, sm, k, q, row, e, wq);
+            else eval_row<N>(S, sm, k, q, row, e, wq);
+#endif
             if (q < PTS) store_row<N>(sm, k, q, row);
         }
         __syncthreads();
@@ -1911,9 +2054,17 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
 // lane mapping (lane = i * PPW + q) with the tracker's state machine per warp -- each warp runs
 // PPW path slots on its own (no CTA barriers); the warps of a CTA share the exp/cis tables and the
 // term records (shared memory, loaded once).  Same control flow as k_track (trk_decide).
-template <int N>
+// LPR = lanes per row: with few paths the tracker is latency-bound (one warp per SMSP), so each
+// row's term loop is split over LPR lanes (terms t = h, h + LPR, ...) whose partial rows are
+// combined with shuffles; the duplicated rows then run the same solve (bitwise identical).
+template <int N, int LPR>
+struct GeoTW {
+    static constexpr int PPW = (N * LPR <= 32) ? 32 / (N * LPR) : 1; // paths (slots) per warp
+};
+
+template <int N, int LPR = 1>
 struct TrackW {
-    static constexpr int PPW = GeoW<N>::PPW;
+    static constexpr int PPW = GeoTW<N, LPR>::PPW;
     double2 rt[N][PPW];                 // (rho, vartheta) of the query points
     double2 xa[N][PPW], xt[N][PPW];     // accepted and trial points
     double2 dd[N][PPW];                 // direction of this iteration
@@ -1926,45 +2077,62 @@ struct TrackW {
     int phase[PPW], it[PPW], succ[PPW], cell[PPW], acc[PPW], refill[PPW], has_prev[PPW], st[PPW];
 };
 
-template <int N>
+template <int N, int LPR = 1>
 struct SmemTW {
     double exptab[TAB_E];
     double2 cistab[TAB_C];
-    TrackW<N> w[GeoW<N>::WARPS];
+    TrackW<N, LPR> w[GeoW<N>::WARPS];
     int mk[N], off[N + 1];
-    // followed by the records R[MT][N][rec_stride(N) / 2]
+    // followed by the records R[MT][N][RecW<N>::U] (16-byte units)
 };
 
 // row k of group point q for the tracker: records from shared memory; cell mode replaces each
-// term's omega by the path's shifted lifting wq[global term index]
-template <int N>
-__device__ __forceinline__ void eval_row_tw(const SmemTW<N> &sm, const double2 *R, const TrackW<N> &W, int k, int q,
-                                            const double *wq, double2 (&row)[N + 2], int &e)
+// term's omega by the path's shifted lifting wq[global term index].  Lane h of the LPR lanes of
+// the row takes the terms h, h + LPR, ...; the partial rows (each with its own binary row
+// exponent) are aligned to the larger exponent and summed across the LPR lanes (shfl_xor).
+// COMP: compensated stage 2 (phi_theta_c) for the final refinement at t = 1 (reading R30).
+template <int N, int LPR, bool COMP = false>
+__device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const double2 *R, const TrackW<N, LPR> &W,
+                                            int k, int q, int h, const double *wq, double2 (&row)[N + 2], int &e)
 {
-    constexpr int RS = rec_stride(N), PPW = GeoW<N>::PPW;
+    constexpr int RS = rec_stride(N), PPW = GeoTW<N, LPR>::PPW;
     PointLog<N, true> pl;
     pl.base = &W.rt[0][q];
     pl.stride = PPW;
     const double tau = W.tau[q];
     const int m = sm.mk[k];
-    const double2 *rec = R + (size_t)k * (RS / 2);
-    constexpr size_t TS = (size_t)N * (RS / 2);
+    const double2 *rec = R + (size_t)k * RecW<N>::U;
+    constexpr size_t TS = (size_t)N * RecW<N>::U;
     const double *wk = wq ? wq + sm.off[k] : nullptr;
     RowAcc<N> acc;
-    {
+    if (h < m) {
         double a[RS];
-        load_rec_s<N>(rec, a);
-        if (wk) a[N] = __ldg(wk);
+        load_rec_s<N>(rec + (size_t)h * TS, a);
+        if (wk) a[N] = __ldg(wk + h);
         acc.init(phi_of<N>(a, pl, tau));
+    } else { // no term on this lane: an empty partial row far below any real one
+        acc.init(0.0);
+        acc.set_exp(-1e6);
     }
-    int i = 0;
-    for (; PHT_PAIR(N) && i + 1 < m; i += 2) {
+    int i = h;
+    if (COMP) {
+        for (; i < m; i += LPR) {
+            double a[RS];
+            load_rec_s<N>(rec + (size_t)i * TS, a);
+            if (wk) a[N] = __ldg(wk + i);
+            double ph, pl_, th, tl;
+            phi_theta_c<N>(a, pl, tau, ph, pl_, th, tl);
+            acc.reduce(ph + pl_);
+            acc.add(a, expcis<true>(acc.reduced2(ph, pl_), th, sm.exptab, sm.cistab, tl));
+        }
+    }
+    for (; PHT_PAIR(N) && i + LPR < m; i += 2 * LPR) {
         double a[RS], b[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
-        load_rec_s<N>(rec + (size_t)(i + 1) * TS, b);
+        load_rec_s<N>(rec + (size_t)(i + LPR) * TS, b);
         if (wk) {
             a[N] = __ldg(wk + i);
-            b[N] = __ldg(wk + i + 1);
+            b[N] = __ldg(wk + i + LPR);
         }
         double pa, pb, ta, tb;
         phi_theta<N>(a, pl, tau, pa, ta);
@@ -1977,7 +2145,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N> &sm, const double2 *
         acc.add(a, wa);
         acc.add(b, wb);
     }
-    for (; i < m; ++i) {
+    for (; i < m; i += LPR) {
         double a[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
         if (wk) a[N] = __ldg(wk + i);
@@ -1990,31 +2158,50 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N> &sm, const double2 *
     for (int j = 0; j < N; ++j) row[j] = acc.g[j];
     row[N] = acc.gt;
     row[N + 1] = acc.h;
-    e = (int)acc.ed;
+    double ed = acc.ed;
+#pragma unroll
+    for (int off = 1; off < LPR; off <<= 1) {
+        // align to the larger row exponent (two normal power-of-two factors, see RowAcc::reduce),
+        // then add the partner's partial row
+        const double eo = __shfl_xor_sync(0xffffffffu, ed, off), em = fmax(ed, eo);
+        const int d = (int)fmax(ed - em, -2000.0), d1 = d / 2;
+        const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d - d1);
+#pragma unroll
+        for (int c = 0; c < N + 2; ++c) {
+            const double2 v = make_double2(row[c].x * f1 * f2, row[c].y * f1 * f2);
+            row[c] = make_double2(v.x + __shfl_xor_sync(0xffffffffu, v.x, off),
+                                  v.y + __shfl_xor_sync(0xffffffffu, v.y, off));
+        }
+        ed = em;
+    }
+    e = (int)ed;
 }
 
-template <int N, bool LOGS>
+template <int N, bool LOGS, int LPR>
 __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const DevSys S, const TrackArgs A, int MT)
 {
     using G = GeoW<N>;
-    constexpr int RS = rec_stride(N), PPW = G::PPW;
+    constexpr int RS = rec_stride(N), PPW = GeoTW<N, LPR>::PPW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SmemTW<N> &sm = *reinterpret_cast<SmemTW<N> *>(smem_raw);
-    double2 *R = reinterpret_cast<double2 *>(smem_raw + ((sizeof(SmemTW<N>) + 15) & ~(size_t)15));
+    SmemTW<N, LPR> &sm = *reinterpret_cast<SmemTW<N, LPR> *>(smem_raw);
+    double2 *R = reinterpret_cast<double2 *>(smem_raw + ((sizeof(SmemTW<N, LPR>) + 15) & ~(size_t)15));
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     const TrackOpts &o = A.o;
     load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
-    for (int idx = tid; idx < MT * N * (RS / 2); idx += G::NT) { // records, term-major
-        const int u = idx % (RS / 2), kk = (idx / (RS / 2)) % N, t = idx / ((RS / 2) * N);
+    for (int idx = tid; idx < MT * N; idx += G::NT) { // records, term-major (only t < m_k is read)
+        const int kk = idx % N, t = idx / N;
         const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
-        R[idx] = (t < m) ? __ldg(S.rec + (size_t)(i0 + t) * (RS / 2) + u) : make_double2(0.0, 0.0);
+        if (t < m) pack_rec_w<N>(S.rec + (size_t)(i0 + t) * (RS / 2), R + (size_t)idx * RecW<N>::U);
     }
     if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
     if (tid <= N) sm.off[tid] = __ldg(S.off + tid);
-    TrackW<N> &W = sm.w[wi];
-    const bool inseg = lane < N * PPW;
-    const int q = inseg ? lane % PPW : 0, i = inseg ? lane / PPW : 0; // lane = i * PPW + q
+    TrackW<N, LPR> &W = sm.w[wi];
+    // lane = (i * PPW + q) * LPR + h: row / variable i of slot q, term share h of that row
+    const bool inseg = lane < N * PPW * LPR;
+    const int gl = lane / LPR, h = lane % LPR;
+    const int q = inseg ? gl % PPW : 0, i = inseg ? gl / PPW : 0;
     const int seg0 = inseg ? q : PPW;
+    const bool prim = inseg && h == 0; // the lane that owns row / variable i of slot q
     if (lane < PPW) {
         W.done_path[lane] = -1;
         W.cell[lane] = 0;
@@ -2025,7 +2212,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
     for (;;) {
         // (1) write back finished paths, accept trial points, load new paths; the query point
         double2 xv = make_double2(LOGS ? 0.0 : 1.0, 0.0);
-        if (inseg) {
+        if (prim) {
             if (W.acc[q]) W.xa[i][q] = W.xt[i][q];
             if (W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
             if (W.refill[q]) W.xa[i][q] = A.x[W.path[q] * N + i];
@@ -2044,7 +2231,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
         }
         __syncwarp();
         // (2) stage 1 for variable i, row i, solve (lane (i, q) ends with variable col)
-        {
+        if (prim) {
             double rho, th;
             int st = 0;
             if (LOGS) {
@@ -2058,35 +2245,41 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
                 double2 iv;
                 log_split(xv, rho, th, iv, st);
             }
-            if (inseg) W.rt[i][q] = make_double2(rho, th);
-            if (st && inseg) atomicOr(&W.st[q], st);
+            W.rt[i][q] = make_double2(rho, th);
+            if (st) atomicOr(&W.st[q], st);
         }
         __syncwarp();
         {
             double2 a[N + 2];
             int e;
             const double *wq = A.cellw ? A.cellw + (size_t)W.cell[q] * A.M : nullptr;
-            eval_row_tw<N>(sm, R, W, i, q, wq, a, e);
+            // the final refinement at t = 1 evaluates with the compensated stage 2 (reading R30):
+            // warp-uniform choice, a few % of the iterations
+            if (__any_sync(0xffffffffu, lane < PPW && W.phase[lane] == PH_FINAL))
+                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e);
+            else
+                eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e);
             normalize_row<N>(a);
             int col;
             double2 dE, dN;
             bool sing;
-            lsolve_regs<N, PPW, G::KS>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, inseg, col, dE, dN, sing);
-            if (inseg) {
+            lsolve_regs<N, PPW, G::KS, true, LPR>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, inseg, col, dE,
+                                                  dN, sing, prim);
+            if (prim) {
                 if (sing) atomicOr(&W.st[q], PT_SINGULAR);
                 W.dd[col][q] = (W.phase[q] == PH_PREDICT) ? dE : dN;
             }
         }
         __syncwarp();
         // (3) element-parallel updates (lane (i, q): variable i of slot q)
-        if (inseg) {
+        if (prim) {
             const int ph = W.phase[q];
             if (W.st[q] == 0 && ph != PH_IDLE) {
                 const double2 dl = W.dd[i][q];
                 if (ph == PH_PREDICT) {
-                    const double h = fmin(W.dt[q], -W.tau_a[q]);
-                    W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], dl, h)
-                                            : trk_update<N, LOGS>(W.xa[i][q], dl, h);
+                    const double hh = fmin(W.dt[q], -W.tau_a[q]);
+                    W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], dl, hh)
+                                            : trk_update<N, LOGS>(W.xa[i][q], dl, hh);
                 } else if (ph == PH_CORRECT) {
                     const double2 v = W.xt[i][q];
                     W.xt[i][q] = trk_update<N, LOGS>(v, dl, 1.0);
@@ -2104,8 +2297,8 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
         __syncwarp();
         const bool busy = __any_sync(0xffffffffu, lane < PPW && W.phase[lane] != PH_IDLE);
         if (!busy) {
-            if (inseg && W.acc[q]) W.xa[i][q] = W.xt[i][q]; // accepted in the last iteration (MAX_STEPS)
-            if (inseg && W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
+            if (prim && W.acc[q]) W.xa[i][q] = W.xt[i][q]; // accepted in the last iteration (MAX_STEPS)
+            if (prim && W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
             break;
         }
     }
@@ -2119,29 +2312,50 @@ bool trackw_eligible(const DevSys &S, const TrackArgs &A)
     return N <= 12 && !S.proj && A.solver == SOLVER_LU && A.o.predictor != 1 && S.mt > 0;
 }
 
-template <int N, bool LOGS>
-cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+template <int N, bool LOGS, int LPR>
+cudaError_t launch_trackw_l(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
-    constexpr int PPW = GeoW<N>::PPW;
-    const size_t sb = ((sizeof(SmemTW<N>) + 15) & ~(size_t)15) + (size_t)S.mt * N * rec_stride(N) * sizeof(double);
+    constexpr int PPW = GeoTW<N, LPR>::PPW;
+    const size_t sb = ((sizeof(SmemTW<N, LPR>) + 15) & ~(size_t)15) + (size_t)S.mt * N * RecW<N>::U * 16;
     if (sb > 200 * 1024) return cudaErrorNotSupported;
     static std::atomic<int64_t> conf_sb[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if ((int64_t)sb > conf_sb[dev & 63].load()) {
-        cudaError_t e = cudaFuncSetAttribute(k_trackw<N, LOGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        cudaError_t e = cudaFuncSetAttribute(k_trackw<N, LOGS, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
         if (e != cudaSuccess) return e;
         conf_sb[dev & 63].store((int64_t)sb);
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trackw<N, LOGS>, GeoW<N>::NT, sb);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trackw<N, LOGS, LPR>, GeoW<N>::NT, sb);
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)sms * per_sm;
     const int64_t need = (A.P + (int64_t)PPW * GeoW<N>::WARPS - 1) / ((int64_t)PPW * GeoW<N>::WARPS);
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    k_trackw<N, LOGS><<<dim3((unsigned)grid), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
+    k_trackw<N, LOGS, LPR><<<dim3((unsigned)grid), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
     return cudaGetLastError();
+}
+
+// Lanes per row of k_trackw: when every path gets its own slot in one wave with LPR = 2 (or 4)
+// lanes per row, the per-iteration latency of the row loop (the time to the last path at small
+// path counts, katsura-10: 990 paths) shrinks; otherwise one lane per row (throughput).
+#ifndef PHT_TRACKW_LPR
+#define PHT_TRACKW_LPR 0 // 0: automatic; 1, 2, 4: forced (experiments)
+#endif
+template <int N, bool LOGS>
+cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
+{
+    const int64_t slots_per_sm = (int64_t)GeoW<N>::WARPS * GeoW<N>::MINB; // warps resident per SM
+    int lpr = PHT_TRACKW_LPR;
+    if (lpr == 0) {
+        lpr = 1;
+        if (N * 4 <= 32 && (A.P + GeoTW<N, 4>::PPW - 1) / GeoTW<N, 4>::PPW <= sms * slots_per_sm) lpr = 4;
+        else if (N * 2 <= 32 && (A.P + GeoTW<N, 2>::PPW - 1) / GeoTW<N, 2>::PPW <= sms * slots_per_sm) lpr = 2;
+    }
+    if (lpr == 4 && N * 4 <= 32) return launch_trackw_l<N, LOGS, (N * 4 <= 32 ? 4 : 1)>(S, A, stream, sms);
+    if (lpr >= 2 && N * 2 <= 32) return launch_trackw_l<N, LOGS, (N * 2 <= 32 ? 2 : 1)>(S, A, stream, sms);
+    return launch_trackw_l<N, LOGS, 1>(S, A, stream, sms);
 }
 
 template <int N, bool LOGS>
@@ -2260,7 +2474,7 @@ cudaError_t launch_stepw(const DevSys &S, const Args &A, cudaStream_t stream)
     constexpr int PPW = GeoW<N>::PPW;
     const int64_t groups = (A.P + PPW - 1) / PPW;
     if (groups == 0) return cudaSuccess;
-    const size_t sb = ((sizeof(SmemW<N>) + 15) & ~(size_t)15) + (size_t)S.mt * N * rec_stride(N) * sizeof(double);
+    const size_t sb = ((sizeof(SmemW<N>) + 15) & ~(size_t)15) + (size_t)S.mt * N * RecW<N>::U * 16;
     if (sb > 200 * 1024) return cudaErrorNotSupported;
     // per device: the largest shared-memory size configured so far and the grid for the last size
     static std::atomic<int64_t> conf_sb[64], last_sb[64], last_fg[64];

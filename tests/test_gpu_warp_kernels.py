@@ -102,7 +102,7 @@ def test_trackw_equals_tile_tracker(P, name, L):
         st, stats = g.track_cells(zd, td, Wc, _cuda(ids))
         res.append((zd.cpu().numpy(), st.cpu().numpy()))
     (zw, sw), (zt, stt) = res
-    assert np.array_equal(sw, stt) and np.sum((sw == 0) | (sw == P.PT_FLOOR)) == len(z)   # finite: OK or FLOOR
+    assert np.array_equal(sw, stt) and np.sum(sw == 0) == len(z)
     xw, xt = np.exp(zw), np.exp(zt)
     assert (np.linalg.norm(xw - xt, axis=1) / np.linalg.norm(xt, axis=1)).max() <= 1e-10
 

@@ -86,6 +86,56 @@ __global__ void k_dmma(double *out, int iters)
     if (s == 123.456) out[0] = s;
 }
 
+// conversion throughput: int32 -> double (I2F.F64), float -> double (F2F.F64.F32), and the
+// magic-number int -> double (IADD + DADD), ILP 8 independent chains
+template <int KIND>
+__global__ void k_conv(double *out, int iters)
+{
+    int iv[8];
+    float fv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { iv[i] = threadIdx.x + i; fv[i] = 0.5f * (threadIdx.x + i); }
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            double d;
+            if (KIND == 0) d = (double)iv[i];
+            else if (KIND == 1) d = (double)fv[i];
+            else d = __hiloint2double(0x43380000, iv[i] + 0x7fffffff) - 6755401602162687.0; // 2^52+2^51 bias
+            acc[i] += d;
+            iv[i] += 3;
+            fv[i] += 1.0f;
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 123.456) out[0] = s;
+}
+
+// shared-memory LDS.128 with DISTINCT 16-byte addresses per warp (1, 3, 8, 32): cycles per warp load
+template <int DISTINCT>
+__global__ void k_lds(double *out, int iters)
+{
+    __shared__ double2 buf[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) buf[i] = make_double2(i, -i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    int idx = (lane % DISTINCT) * 7 % 1024;     // stride 7 (odd): distinct banks
+    double2 acc = make_double2(0, 0);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double2 v = buf[(idx + u * 64) & 1023];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        idx = (idx + 8) & 1023;
+    }
+    if (acc.x == 123.456) out[0] = acc.y;
+}
+
 int main()
 {
     double *d;
@@ -229,6 +279,44 @@ int main()
         // half of each workload together vs the sum of the halves alone (ms_m/2 + ms_f/2)
         printf(", \"coissue\": {\"dmma_ms\": %.3f, \"dfma_ms\": %.3f, \"half_each_concurrent_ms\": %.3f, "
                "\"half_each_serial_ms\": %.3f}", ms_m, ms_f, ms_b, 0.5 * (ms_m + ms_f));
+    }
+    // conversions (G ops per second over the whole GPU)
+    {
+        const char *names[3] = {"i2f_f64", "f2f_f64_f32", "magic_int_to_f64"};
+        printf(", \"conversions_G_per_s\": {");
+        for (int kind = 0; kind < 3; ++kind) {
+            const int iters = 20000, blocks = sms * 4, threads = 256;
+            void (*k)(double *, int) = kind == 0 ? k_conv<0> : (kind == 1 ? k_conv<1> : k_conv<2>);
+            k<<<blocks, threads>>>(d, 10);
+            cudaEventRecord(e0);
+            k<<<blocks, threads>>>(d, iters);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("%s\"%s\": %.1f", kind ? ", " : "", names[kind], 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e9);
+        }
+        printf("}");
+    }
+    // LDS.128: warp loads per SM per cycle, by distinct addresses in the warp
+    {
+        printf(", \"lds128_warp_loads_per_sm_cycle\": {");
+        const int ds[4] = {1, 3, 8, 32};
+        for (int u = 0; u < 4; ++u) {
+            const int iters = 20000, blocks = sms * 4, threads = 256;
+            void (*k)(double *, int) = u == 0 ? k_lds<1> : (u == 1 ? k_lds<3> : (u == 2 ? k_lds<8> : k_lds<32>));
+            k<<<blocks, threads>>>(d, 10);
+            cudaEventRecord(e0);
+            k<<<blocks, threads>>>(d, iters);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double loads = 8.0 * iters * (double)blocks * (threads / 32);
+            const double cyc = ms * 1e-3 * mhz * 1e3 * sms;
+            printf("%s\"%d\": %.3f", u ? ", " : "", ds[u], loads / cyc);
+        }
+        printf("}");
     }
     printf("}\n");
     return 0;
