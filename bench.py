@@ -248,6 +248,7 @@ def evaluation_section(world, rank, dev, reps=5):
         if name.endswith("specialised"):
             t0 = time.perf_counter()
             g.specialize()  # NVRTC compile of the generated rows: outside the timed region
+            g.set_kernels("specialized")   # (AUTO would take the faster generic k_evalw)
             spec_s = time.perf_counter() - t0
         x, t, _ = W.random_points(Pn, sysm.n, seed=2000 + rank, rho_max=0.5 if sysm.n > 12 else 1.0)
         xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
@@ -281,8 +282,9 @@ def evaluation_section(world, rank, dev, reps=5):
                               "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak_tflops(1965.0),
                               "flops_per_point": fl / Pn},
                      "path": ("system-specialised point-per-thread kernel (NVRTC)" if spec_s is not None else
-                              "FP64 tensor cores (DMMA)" if (g.dense and n >= 11) else
-                              "warp-per-group kernel k_stepw<N, EVAL_X>" if n <= 10 else "scalar FP64 kernel")}
+                              "FP64 tensor cores (DMMA, k_dense)" if n > 12 else
+                              "point-per-lane kernel k_evalw (TMA tensor stores)" if n >= 6 else
+                              "warp-per-group kernel k_stepw<N, EVAL_X>")}
         if spec_s is not None:
             out[name]["specialize_s"] = spec_s
         del g, xd, td, H, J, Jt, st

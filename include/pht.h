@@ -194,6 +194,9 @@ int pht_system_set_solver(pht_system *sys, int32_t solver);
  *                               systems); AUTO for the other entry points.
  *   PHT_KERNELS_SPECIALIZED     the system-specialised kernels for every entry point they were
  *                               compiled for (PHT_EUNSUPPORTED before pht_system_specialize).
+ *   PHT_KERNELS_LANE            pht_evaluate / pht_evaluate_log on the point-per-lane kernel (a warp
+ *                               owns 32 points and walks the equations; rows leave through TMA
+ *                               tensor stores), n <= 12; AUTO for the other entry points.
  * Host-synchronous (PHT_KERNELS_DENSE may upload tables); not synchronised with calls in flight.
  * Returns PHT_OK, PHT_EINVAL, PHT_EUNSUPPORTED, PHT_ENOMEM or PHT_ECUDA.  pht_system_kernels
  * returns the current family.
@@ -203,6 +206,7 @@ int pht_system_set_solver(pht_system *sys, int32_t solver);
 #define PHT_KERNELS_WARP 2
 #define PHT_KERNELS_DENSE 3
 #define PHT_KERNELS_SPECIALIZED 4
+#define PHT_KERNELS_LANE 5
 int pht_system_set_kernels(pht_system *sys, int32_t family);
 int pht_system_kernels(const pht_system *sys);
 

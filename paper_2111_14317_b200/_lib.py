@@ -19,7 +19,7 @@ PT_STEP_UNDERFLOW, PT_MAX_STEPS, PT_DIVERGED, PT_FLOOR = 8, 16, 32, 64
 SYS_DENSE, SYS_SPECIALIZED, SYS_PROJECTIVE = 1, 2, 4
 SPEC_EVAL, SPEC_STEP, SPEC_TRACK, SPEC_ALL = 1, 2, 4, 7
 SOLVER_LU, SOLVER_QR = 0, 1
-KERNELS = {"auto": 0, "tile": 1, "warp": 2, "dense": 3, "specialized": 4}   # PHT_KERNELS_*
+KERNELS = {"auto": 0, "tile": 1, "warp": 2, "dense": 3, "specialized": 4, "lane": 5}   # PHT_KERNELS_*
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32

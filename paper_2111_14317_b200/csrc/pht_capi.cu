@@ -2,8 +2,11 @@
 // paper's Alg. 1 "Initialize") and the entry points that enqueue k_pht.
 #include "../../include/pht.h"
 #include "pht_dense.cuh"
+#include "pht_evalw.cuh"
 #include "pht_jit.h"
 #include "pht_kernels.cuh"
+
+#include <cudaTypedefs.h> // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
 
 #include <algorithm>
 #include <cstdint>
@@ -22,12 +25,54 @@ namespace pht {
 #define PHT_DECL(N)                                                                             \
     extern template cudaError_t launch<N>(int, const DevSys &, const Args &, cudaStream_t, int); \
     extern template cudaError_t launch_track<N>(const DevSys &, const TrackArgs &, cudaStream_t, int, int); \
-    extern template cudaError_t launch_dense<N>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t);
+    extern template cudaError_t launch_dense<N>(int, const DevSys &, const DenseSys &, const Args &, cudaStream_t); \
+    extern template cudaError_t launch_evalw<N, MODE_EVAL_X>(const DevSys &, const Args &, const EvalMaps &, cudaStream_t); \
+    extern template cudaError_t launch_evalw<N, MODE_EVAL_Z>(const DevSys &, const Args &, const EvalMaps &, cudaStream_t);
 PHT_DECL(1) PHT_DECL(2) PHT_DECL(3) PHT_DECL(4) PHT_DECL(5) PHT_DECL(6) PHT_DECL(7) PHT_DECL(8)
 PHT_DECL(9) PHT_DECL(10) PHT_DECL(11) PHT_DECL(12) PHT_DECL(13) PHT_DECL(14) PHT_DECL(15)
 PHT_DECL(16) PHT_DECL(17) PHT_DECL(18) PHT_DECL(19) PHT_DECL(20) PHT_DECL(21) PHT_DECL(22)
 PHT_DECL(23) PHT_DECL(24)
 #undef PHT_DECL
+
+// TMA tensor maps of the evaluation outputs (k_evalw): Jx as [P][n][2n] doubles with box {2n, 1, 32},
+// Jt and H as [P][n][2] with box {2, 1, 32}.  The encoder comes from the driver through the runtime's
+// entry-point query (the library links no libcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder()
+{
+    static std::once_flag once;
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+static bool encode3(CUtensorMap *m, void *base, int64_t d0, int64_t d1, int64_t d2, uint32_t b0)
+{
+    const cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+    const cuuint64_t strides[2] = {(cuuint64_t)(d0 * 8), (cuuint64_t)(d0 * d1 * 8)};
+    const cuuint32_t box[3] = {b0, 1, 32}, estr[3] = {1, 1, 1};
+    return tmap_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int encode_eval_maps(EvalMaps &M, int n, int64_t P, void *J, void *Jt, void *H)
+{
+    M.tma = 0;
+    if (!tmap_encoder() || P <= 0 || P > ((int64_t)1 << 31)) return 0;
+    for (void *ptr : {J, Jt, H})
+        if (ptr && ((uintptr_t)ptr & 15u)) return 0;
+    if (J && !encode3(&M.J, J, 2 * n, n, P, (uint32_t)(2 * n))) return 0;
+    if (Jt && !encode3(&M.T, Jt, 2, n, P, 2)) return 0;
+    if (H && !encode3(&M.H, H, 2, n, P, 2)) return 0;
+    M.tma = 1;
+    return 1;
+}
 } // namespace pht
 
 static_assert(PHT_MAX_N == 24, "dispatch table below covers n = 1..24");
@@ -376,7 +421,7 @@ extern "C" int pht_system_set_solver(pht_system *s, int32_t solver)
 
 extern "C" int pht_system_set_kernels(pht_system *s, int32_t family)
 {
-    if (!s || family < PHT_KERNELS_AUTO || family > PHT_KERNELS_SPECIALIZED) return PHT_EINVAL;
+    if (!s || family < PHT_KERNELS_AUTO || family > PHT_KERNELS_LANE) return PHT_EINVAL;
     if (family == PHT_KERNELS_DENSE) {
         if (s->proj) return PHT_EUNSUPPORTED;
         const int rc = build_dense(s);
@@ -528,7 +573,9 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     bool use_jit = false;
     if (jit_ok) {
         if (fam == PHT_KERNELS_SPECIALIZED) use_jit = true;
-        else if (fam == PHT_KERNELS_AUTO) use_jit = evalm || !warp_step;
+        // AUTO: the generic point-per-lane evaluation (k_evalw, 6 <= n <= 12) beats the specialised
+        // evaluation (cyclic-10 1.06 vs 0.81 G points/s); the specialised step below n = 10
+        else if (fam == PHT_KERNELS_AUTO) use_jit = evalm ? (s->n < 6 || s->n > 12 || s->proj) : !warp_step;
     }
     if (use_jit) {
         e = pht::jit_launch(J, mode, S, A, st);
@@ -539,11 +586,38 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     bool dense = false;
     if (evalm && s->dense) {
         if (fam == PHT_KERNELS_DENSE) dense = true;
-        else if (fam == PHT_KERNELS_AUTO || fam == PHT_KERNELS_SPECIALIZED)
-            dense = s->n >= 11 || mode == pht::MODE_EVAL_Z;
+        else if (fam == PHT_KERNELS_AUTO || fam == PHT_KERNELS_SPECIALIZED) dense = s->n > 12;
     }
     const int lfam = fam == PHT_KERNELS_TILE ? pht::FAM_TILE : pht::FAM_AUTO;
     const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff, s->max_ntk};
+    // point-per-lane evaluation (k_evalw): LANE for n <= 12, AUTO for 6 <= n <= 12 (measured, one B200,
+    // G points/s: cyclic-10 1.06 vs 0.76 warp-per-group vs 0.62 tensor cores, noon-10 0.96 / 0.71 /
+    // 0.61, katsura-10 (n = 11) 0.70 / 0.44 / 0.58; cyclic-5 2.85 vs 3.31 for the warp-per-group
+    // kernel, which stays the AUTO choice for pht_evaluate below n = 6; pht_evaluate_log: cyclic-5 2.92
+    // vs 2.77 tile); PHT_KERNELS_WARP keeps k_stepw<N, EVAL_X>
+    const bool lane_eval = evalm && !s->proj && s->n <= 12 && s->max_terms > 0 && !dense &&
+                           (fam == PHT_KERNELS_LANE ||
+                            ((fam == PHT_KERNELS_AUTO || fam == PHT_KERNELS_SPECIALIZED) &&
+                             (s->n >= 6 || mode == pht::MODE_EVAL_Z)));
+    if (lane_eval) {
+        pht::EvalMaps M{};
+        pht::encode_eval_maps(M, s->n, A.P, A.J, A.Jt, A.H);
+        e = cudaErrorNotSupported;
+        switch (s->n) {
+#define PHT_CASE(N) case N: e = mode == pht::MODE_EVAL_X ? pht::launch_evalw<N, pht::MODE_EVAL_X>(S, A, M, st) \
+                                                        : pht::launch_evalw<N, pht::MODE_EVAL_Z>(S, A, M, st); break;
+            PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)
+            PHT_CASE(8) PHT_CASE(9) PHT_CASE(10) PHT_CASE(11) PHT_CASE(12)
+#undef PHT_CASE
+        default: break;
+        }
+        if (e != cudaErrorNotSupported) {
+            if (e != cudaSuccess) return cuda_fail(e);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            return PHT_OK;
+        }
+        cudaGetLastError(); // (too many terms for shared memory: the kernels below)
+    }
     switch (s->n) {
 #define PHT_CASE(N) case N: e = dense ? pht::launch_dense<N>(mode, S, D, A, st) : pht::launch<N>(mode, S, A, st, lfam); break;
         PHT_CASE(1) PHT_CASE(2) PHT_CASE(3) PHT_CASE(4) PHT_CASE(5) PHT_CASE(6) PHT_CASE(7)

@@ -88,7 +88,7 @@ def test_log_branch_invariance(P):
     assert np.allclose(a[1].cpu().numpy() * sa, b[1].cpu().numpy() * sa, rtol=1e-13, atol=1e-13 * np.abs(a[1].cpu().numpy() * sa).max())
 
 
-FAMILIES_LOG = ["tile", "dense", "specialized"]   # every kernel that implements pht_evaluate_log
+FAMILIES_LOG = ["tile", "dense", "specialized", "lane"]   # every kernel that implements pht_evaluate_log
 
 
 def _log_family(P, sysm, family):
@@ -309,7 +309,7 @@ def test_dense_tensor_core_evaluate(P, n, m, p):
     assert be[st2.cpu().numpy() == 0].max() <= 1e-10
 
 
-@pytest.mark.parametrize("family", ["tile", "dense", "specialized"])
+@pytest.mark.parametrize("family", ["tile", "dense", "specialized", "lane"])
 def test_row_rescale_keeps_entries_far_below_the_row(P, family):
     """Regression (found by the C5 range-stress test): the online row rescale by 2^d with
     d < -1074 must not flush entries that stay representable.  h_1 = 1 + x1 + x2^2 at

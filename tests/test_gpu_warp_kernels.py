@@ -127,22 +127,23 @@ def test_stepw_directions_equal_tile_kernel(P, name, p):
 
 @pytest.mark.parametrize("name,p", [("cyclic-5", 777), ("chandra-6", 517), ("cyclic-7", 1001), ("cyclic-10", 2003), ("noon-10", 301), ("n1", 65)])
 def test_evaluate_warp_kernel_equals_tile_kernel(P, name, p):
-    """pht_evaluate through k_stepw<N, EVAL_X> (the default for 6 <= n <= 10) equals the tile
-    kernel k_phte, unscaled and with row exponents (the same row arithmetic)."""
+    """pht_evaluate through k_stepw<N, EVAL_X>, the tile kernel k_phte and the point-per-lane kernel
+    k_evalw (TMA stores) agree, unscaled and with row exponents (the same row arithmetic)."""
     sysm = SYS[name]()
     g = P.System.from_workload(sysm)
     x, t, _ = W.random_points(p, sysm.n, seed=35)
     for scaled in (False, True):
         out = []
-        for fam in ("warp", "tile"):
+        for fam in ("warp", "tile", "lane"):
             g.set_kernels(fam)
             r = g.evaluate(_cuda(x), _cuda(t), scaled=scaled)
             out.append([a.cpu().numpy() for a in r])
-        for a, b in zip(*out):
-            if a.dtype == np.complex128:
-                assert np.allclose(a, b, rtol=1e-13, atol=0) or np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-13
-            else:
-                assert np.array_equal(a, b)
+        for other in out[1:]:
+            for a, b in zip(out[0], other):
+                if a.dtype == np.complex128:
+                    assert np.allclose(a, b, rtol=1e-13, atol=0) or np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-13
+                else:
+                    assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("m", [300, 420])

@@ -11,13 +11,14 @@ mkdir -p build_var/$name ../lib_$name
 objs=""
 for o in build/*.o; do
   keep=1
-  for n in $ns; do [ "$o" == "build/inst_n$n.o" ] && keep=0; done
+  for n in $ns; do [ "$o" == "build/inst_n$(printf %02d $n).o" ] && keep=0; done
   [ $keep == 1 ] && objs="$objs $o"
 done
 pids=""
 for n in $ns; do
-  $NV $flags -c inst_n$n.cu -o build_var/$name/inst_n$n.o & pids="$pids $!"
-  objs="$objs build_var/$name/inst_n$n.o"
+  nn=$(printf %02d $n)
+  $NV $flags -c inst_n$nn.cu -o build_var/$name/inst_n$nn.o & pids="$pids $!"
+  objs="$objs build_var/$name/inst_n$nn.o"
 done
 for p in $pids; do wait $p; done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../lib_$name/libpht.so $objs -cudart static -L/usr/local/cuda/lib64 -lnvrtc -Xlinker -rpath -Xlinker /usr/local/cuda/lib64
