@@ -162,9 +162,9 @@ def run_reference(args):
 
 def step_traffic(points):
     """DRAM bytes per step launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
-    ncu --set full capture of the same kernel (profiles/r01_step_traffic.json), scaled from the
+    ncu --set full capture of the same kernel (profiles/r02_step_traffic.json), scaled from the
     captured launch's point count to this launch's; None if the capture is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_step_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_step_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)

@@ -36,6 +36,9 @@ struct EvalMaps {
 #ifndef PHT_EVALW_WARPS
 #define PHT_EVALW_WARPS 12
 #endif
+#ifndef PHT_EVALW_PAIR
+#define PHT_EVALW_PAIR 0 // two terms per iteration in k_evalw's row loop (experiments)
+#endif
 #ifndef PHT_EVALW_MINB
 #define PHT_EVALW_MINB 1
 #endif
@@ -141,7 +144,22 @@ __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
                 load_rec_s<N>(rec, a);
                 acc.init(phi_of<N>(a, pl, tau));
             }
-            for (int i = 0; i < m; ++i) {
+            int i = 0;
+            for (; PHT_EVALW_PAIR && i + 1 < m; i += 2) { // two terms per iteration (ILP)
+                double a[RS], b[RS];
+                load_rec_s<N>(rec + (size_t)i * TS, a);
+                load_rec_s<N>(rec + (size_t)(i + 1) * TS, b);
+                double pa, ta, pb, tb;
+                phi_theta<N>(a, pl, tau, pa, ta);
+                phi_theta<N>(b, pl, tau, pb, tb);
+                acc.reduce(pa);
+                acc.reduce(pb);
+                const double2 wa = expcis(acc.reduced(pa), ta, sm.exptab, sm.cistab);
+                const double2 wb = expcis(acc.reduced(pb), tb, sm.exptab, sm.cistab);
+                acc.add(a, wa);
+                acc.add(b, wb);
+            }
+            for (; i < m; ++i) {
                 double a[RS];
                 load_rec_s<N>(rec + (size_t)i * TS, a);
                 double pa, ta;

@@ -766,7 +766,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src)
     return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-template <int N, int PPW, int KS, bool IMAJ = false, int LPR = 1>
+template <int N, int PPW, int KS, bool IMAJ = false, int LPR = 1, bool SHFL = (bool)PHT_W_SHFL>
 __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, unsigned *kseg, int seg0, int seg,
                                             int i, bool act, int &col, double2 &dE, double2 &dN, bool &singular,
                                             bool prim = true)
@@ -816,7 +816,7 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
             used = true;
             col = j;
         }
-#if PHT_W_SHFL
+        if (SHFL) {
         const int src = IMAJ ? (r * PPW + seg) * LPR : seg * N + r; // a lane holding this point's pivot row
         const double2 rcp = shfl2(crcp, src);
         {
@@ -830,7 +830,7 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
         for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, shfl2(a[c], src));
         a[j] = me ? a[j] : make_double2(0.0, 0.0);
         if (PPW > 4) __syncwarp(); // kseg is rewritten by the next pivot search
-#else
+        } else {
         if (me && act && prim) {
             // the pivot row with the pivot replaced by its reciprocal (computed before the
             // argmax by every lane for its own candidate: the reciprocal's latency overlaps the
@@ -856,7 +856,7 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
         for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, prow[c]);
         a[j] = me ? a[j] : make_double2(0.0, 0.0);
         __syncwarp();
-#endif
+        }
     }
     const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
     dE = make_double2(-e.x, -e.y);
@@ -2057,9 +2057,23 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
 // LPR = lanes per row: with few paths the tracker is latency-bound (one warp per SMSP), so each
 // row's term loop is split over LPR lanes (terms t = h, h + LPR, ...) whose partial rows are
 // combined with shuffles; the duplicated rows then run the same solve (bitwise identical).
+#ifndef PHT_TRACKW_LOWOCC_MINB
+#define PHT_TRACKW_LOWOCC_MINB 4 // resident 4-warp CTAs per SM the LPR > 1 (few-path) tracker is built for
+#endif
+#ifndef PHT_TRACKW_LOWOCC_SHFL
+#define PHT_TRACKW_LOWOCC_SHFL 0 // measured: katsura-10 4.3 ms with shuffles vs 3.8 through shared memory
+#endif
+#ifndef PHT_TRACKW_LOWOCC_PAIR
+#define PHT_TRACKW_LOWOCC_PAIR 0 // LPR > 1: two terms per iteration (ILP) for n <= 12
+#endif
 template <int N, int LPR>
 struct GeoTW {
     static constexpr int PPW = (N * LPR <= 32) ? 32 / (N * LPR) : 1; // paths (slots) per warp
+    static constexpr int MINB = LPR > 1 ? PHT_TRACKW_LOWOCC_MINB : GeoW<N>::MINB;
+    static constexpr bool PAIR = LPR > 1 ? (PHT_TRACKW_LOWOCC_PAIR && N <= 12) : PHT_PAIR(N);
+    // pivot-row broadcast by shuffles in the latency-bound few-path tracker (no shared round trip
+    // and no __syncwarp per pivot), through shared memory in the throughput kernels
+    static constexpr bool SHFL = LPR > 1 ? (bool)PHT_TRACKW_LOWOCC_SHFL : (bool)PHT_W_SHFL;
 };
 
 template <int N, int LPR = 1>
@@ -2126,7 +2140,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
             acc.add(a, expcis<true>(acc.reduced2(ph, pl_), th, sm.exptab, sm.cistab, tl));
         }
     }
-    for (; PHT_PAIR(N) && i + LPR < m; i += 2 * LPR) {
+    for (; GeoTW<N, LPR>::PAIR && i + LPR < m; i += 2 * LPR) {
         double a[RS], b[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
         load_rec_s<N>(rec + (size_t)(i + LPR) * TS, b);
@@ -2178,7 +2192,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
 }
 
 template <int N, bool LOGS, int LPR>
-__global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const DevSys S, const TrackArgs A, int MT)
+__global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(const DevSys S, const TrackArgs A, int MT)
 {
     using G = GeoW<N>;
     constexpr int RS = rec_stride(N), PPW = GeoTW<N, LPR>::PPW;
@@ -2263,8 +2277,8 @@ __global__ void __launch_bounds__(GeoW<N>::NT, GeoW<N>::MINB) k_trackw(const Dev
             int col;
             double2 dE, dN;
             bool sing;
-            lsolve_regs<N, PPW, G::KS, true, LPR>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q, i, inseg, col, dE,
-                                                  dN, sing, prim);
+            lsolve_regs<N, PPW, G::KS, true, LPR, GeoTW<N, LPR>::SHFL>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q,
+                                                                        i, inseg, col, dE, dN, sing, prim);
             if (prim) {
                 if (sing) atomicOr(&W.st[q], PT_SINGULAR);
                 W.dd[col][q] = (W.phase[q] == PH_PREDICT) ? dE : dN;
@@ -2346,7 +2360,8 @@ cudaError_t launch_trackw_l(const DevSys &S, const TrackArgs &A, cudaStream_t st
 template <int N, bool LOGS>
 cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
-    const int64_t slots_per_sm = (int64_t)GeoW<N>::WARPS * GeoW<N>::MINB; // warps resident per SM
+    // warps resident per SM of the LPR > 1 kernels (their register budget: GeoTW::MINB)
+    const int64_t slots_per_sm = (int64_t)GeoW<N>::WARPS * GeoTW<N, 2>::MINB;
     int lpr = PHT_TRACKW_LPR;
     if (lpr == 0) {
         lpr = 1;

@@ -14,7 +14,7 @@ sysm = {"cyclic-10": lambda: W.cyclic(10, lift_max=100), "random-20x50": lambda:
 g = P.System.from_workload(sysm)
 if os.environ.get("PHT_SPEC") == "1":
     g.specialize()
-p = 1 << 20 if sysm.n <= 10 else 1 << 17
+p = 1 << 21 if sysm.n <= 10 else 1 << 20   # the bench.py evaluation sizes
 x, t, _ = W.random_points(p, sysm.n, seed=1, rho_max=0.5 if sysm.n > 12 else 1.0)
 xd, td = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()
 for _ in range(2):
