@@ -91,6 +91,8 @@ struct pht_system {
     int *d_off = nullptr;
     double *d_exptab = nullptr;
     double2 *d_cistab = nullptr;
+    double2 *d_logtab = nullptr; // log_split_t tables (pht_kernels.cuh)
+    double *d_atantab = nullptr;
     // dense FP64 tensor-core path (pht_dense.cuh), built when the system is genuinely dense
     int dense = 0;
     double *d_b2phi = nullptr, *d_b2th = nullptr, *d_b4 = nullptr;
@@ -300,6 +302,15 @@ static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const in
         ctab[2 * j] = (double)cosl(2.0L * PI_L * (long double)j / 256.0L);
         ctab[2 * j + 1] = (double)sinl(2.0L * PI_L * (long double)j / 256.0L);
     }
+    // log / atan tables of log_split_t: (1/c_j rounded, -log of that rounded value) so that
+    // r = m (1/c_j) - 1 carries the rounding of 1/c_j exactly, c_j = 1 + (j + 1/2)/128; atan(k/64)
+    std::vector<double> ltab(256), atab(65);
+    for (int j = 0; j < 128; ++j) {
+        const double ic = (double)(1.0L / (1.0L + ((long double)j + 0.5L) / 128.0L));
+        ltab[2 * j] = ic;
+        ltab[2 * j + 1] = (double)(-logl((long double)ic));
+    }
+    for (int k = 0; k <= 64; ++k) atab[k] = (double)atanl((long double)k / 64.0L);
 
     DevGuard g(device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
@@ -337,7 +348,11 @@ static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const in
         (e = cudaMemcpy(s->d_rec, rec.data(), rec.size() * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(s->d_off, doff.data(), doff.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(s->d_exptab, etab.data(), 256 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaMemcpy(s->d_cistab, ctab.data(), 512 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess) {
+        (e = cudaMemcpy(s->d_cistab, ctab.data(), 512 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_logtab, 128 * sizeof(double2))) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_atantab, 65 * sizeof(double))) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_logtab, ltab.data(), 256 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_atantab, atab.data(), 65 * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess) {
         pht_system_destroy(s);
         return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
     }
@@ -377,6 +392,8 @@ extern "C" void pht_system_destroy(pht_system *s)
     cudaFree(s->d_off);
     cudaFree(s->d_exptab);
     cudaFree(s->d_cistab);
+    cudaFree(s->d_logtab);
+    cudaFree(s->d_atantab);
     cudaFree(s->d_b2phi);
     cudaFree(s->d_b2th);
     cudaFree(s->d_b4);
@@ -559,7 +576,7 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
     if (A0.P == 0) return PHT_OK;
     DevGuard g(s->device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
-    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj, s->max_terms};
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj, s->max_terms, s->d_logtab, s->d_atantab};
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     pht::Args A = A0;
@@ -866,7 +883,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     cudaError_t e;
     if ((e = cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st)) != cudaSuccess) return cuda_fail(e);
-    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj, s->max_terms};
+    pht::DevSys S{s->d_rec, s->d_off, s->d_exptab, s->d_cistab, s->n, s->proj, s->max_terms, s->d_logtab, s->d_atantab};
     pht::TrackArgs A{};
     A.P = p;
     A.x = (double2 *)x;

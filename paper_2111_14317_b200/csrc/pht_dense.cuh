@@ -77,6 +77,14 @@ struct DGeo {
     static constexpr int PTS = WARPS * NMT * 8; // points per CTA
 };
 
+// monotone 32-bit integer key of a double's high word (NaN above +inf) and its inverse (low word 0)
+__device__ __forceinline__ int dkey_hi(double v)
+{
+    const int h = __double2hiint(v);
+    return h ^ ((h >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ double dkey_hi_inv(int k) { return __hiloint2double(k ^ ((k >> 31) & 0x7fffffff), 0); }
+
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
                 }
             } else {
                 double2 inv;
-                log_split(v, rho, th, inv, st);
+                log_split_t(v, rho, th, inv, st, S.logtab, S.atantab);
                 sm.inv[q][j] = inv;
             }
         }
@@ -232,9 +240,14 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
             double wr[NMT][2], wi[NMT][2];
 #pragma unroll
             for (int m = 0; m < NMT; ++m) {
-                double mx = fmax(ph[m][0], ph[m][1]);
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                // row maximum on the integer pipe: the high words of the doubles in a monotone
+                // integer key (sign-magnitude -> two's complement); the row exponent only needs the
+                // maximum to ~2^-20 relative (measured: the FP64 DSETP.MAX chain was the hottest
+                // stall of the kernel, on the datapath DMMA shares)
+                int kx = max(dkey_hi(ph[m][0]), dkey_hi(ph[m][1]));
+                kx = max(kx, __shfl_xor_sync(0xffffffffu, kx, 1));
+                kx = max(kx, __shfl_xor_sync(0xffffffffu, kx, 2));
+                const double mx = dkey_hi_inv(kx);
                 if (ed[m] == -1e300) { // first n-tile: set the exponent from the leading term
                     ed[m] = isfinite(mx) ? rint(mx * KC[14]) : 0.0;
                     eh[m] = ed[m] * KC[12];

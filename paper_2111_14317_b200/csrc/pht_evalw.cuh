@@ -36,6 +36,9 @@ struct EvalMaps {
 #ifndef PHT_EVALW_WARPS
 #define PHT_EVALW_WARPS 12
 #endif
+#ifndef PHT_EVALW_TMA
+#define PHT_EVALW_TMA 1 // 0: direct stores from registers (experiments)
+#endif
 #ifndef PHT_EVALW_PAIR
 #define PHT_EVALW_PAIR 0 // two terms per iteration in k_evalw's row loop (experiments)
 #endif
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
             if (act) v = A.xin[p * N + j];
             if (XM) {
                 double2 iv;
-                log_split(v, pl.rho[j], pl.th[j], iv, st);
+                log_split_t(v, pl.rho[j], pl.th[j], iv, st, S.logtab, S.atantab);
                 W.inv[j][lane] = iv;
             } else if (!(isfinite(v.x) && isfinite(v.y))) {
                 st |= PT_NONFINITE;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
             for (int c = 0; c < N + 2; ++c) fin = fin && isfinite(row[c].x) && isfinite(row[c].y);
             if (!fin) st |= PT_NONFINITE;
             if (act && scaled) A.rexp[p * N + k] = e;
-            if (M.tma) {
+            if (PHT_EVALW_TMA && M.tma) {
                 // the previous row's store must have finished reading the staging buffer
                 if (pending && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();

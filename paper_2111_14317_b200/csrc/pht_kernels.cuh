@@ -62,6 +62,8 @@ struct DevSys {
     int n;
     int proj; // projective system: N = n_eq + 1 homogeneous coordinates, row N-1 = y^*
     int mt;   // most terms of one equation (k_stepw's shared-memory record table)
+    const double2 *logtab; // [128] (1/c_j rounded, -log of it), c_j = 1 + (j + 1/2)/128 (log_split_t)
+    const double *atantab; // [65] atan(k/64)
 };
 
 struct Args {
@@ -271,6 +273,49 @@ __device__ __forceinline__ void log_split(double2 x, double &rho, double &th, do
         inv = crecip(x);
     }
     th = atan2(x.y, x.x);
+}
+
+// a1 with table-driven log and atan2 (about half the FP64 work of libdevice log + atan2; error
+// <= ~1 ulp of max(|log|, 1) and ~1.1 ulp of pi): log s = e ln2 + log c_j + log1p(r)
+// with s = 2^e m, c_j the midpoint of m's 1/128 interval, r = m / c_j - 1 (|r| <= 2^-8, degree-7
+// series); atan(t) for t = min/max in [0, 1] as atan(k/64) + atan((t - t_k) / (1 + t t_k))
+// (|u| <= 2^-7, degree-7 series), then the octant.  Extreme magnitudes take log_split.
+__device__ __forceinline__ void log_split_t(double2 x, double &rho, double &th, double2 &inv, int &st,
+                                            const double2 *logtab, const double *atantab)
+{
+    const double ax = fabs(x.x), ay = fabs(x.y);
+    const double m = fmax(ax, ay);
+    if (!(m > 0x1p-500 && m < 0x1p+500)) { // zero, non-finite or extreme: the general routine
+        log_split(x, rho, th, inv, st);
+        return;
+    }
+    const double s = fma(x.x, x.x, x.y * x.y);
+    const long long bits = __double_as_longlong(s);
+    const int j = (int)(bits >> 45) & 127;
+    const double mm = __longlong_as_double((bits & 0x000fffffffffffffll) | 0x3ff0000000000000ll);
+    const double2 tj = __ldg(logtab + j);
+    const double r = fma(mm, tj.x, -1.0);
+    double q = fma(r, 1.0 / 7.0, -1.0 / 6.0);
+    q = fma(q, r, 0.2);
+    q = fma(q, r, -0.25);
+    q = fma(q, r, 1.0 / 3.0);
+    q = fma(q, r, -0.5);
+    const double ef = (double)((int)(bits >> 52) - 1023);
+    rho = 0.5 * fma(ef, KC[12], tj.y + fma(ef, KC[13], fma(q * r, r, r)));
+    const double is = rcp_nr(s);
+    inv = make_double2(x.x * is, -x.y * is);
+    const bool swap = ay > ax;
+    const double t = (swap ? ax : ay) * rcp_nr(m);
+    const double kd = rint(t * 64.0);
+    const double tk = kd * (1.0 / 64.0);
+    const double u = (t - tk) * rcp_nr(fma(t, tk, 1.0));
+    const double u2 = u * u;
+    double w = fma(u2, -1.0 / 7.0, 0.2);
+    w = fma(w, u2, -1.0 / 3.0);
+    const double at = __ldg(atantab + (int)kd) + fma(w * u2, u, u);
+    double a = swap ? (0x1.921fb54442d18p+0 - at) + 0x1.1a62633145c07p-54 : at; // pi/2 - at
+    a = (x.x < 0.0) ? (0x1.921fb54442d18p+1 - a) + 0x1.1a62633145c07p-53 : a;  // pi - a
+    th = (x.y < 0.0) ? -a : a;
 }
 
 // a3: w = exp(y) * (cos th + i sin th), y <= ~0.35 by construction of the row exponent.
@@ -1211,7 +1256,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_pht(const DevSys S
                     double rho, th;
                     double2 iv;
                     int st = 0;
-                    log_split(xn, rho, th, iv, st);
+                    log_split_t(xn, rho, th, iv, st, S.logtab, S.atantab);
                     sm.rt[col][qq] = make_double2(rho, th);
                     if (st) atomicOr(&sm.st[qq], st);
                 }
@@ -1498,7 +1543,7 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
             double rho, th;
             double2 iv;
             int st = 0;
-            log_split(xv, rho, th, iv, st); // a1 for variable i
+            log_split_t(xv, rho, th, iv, st, S.logtab, S.atantab); // a1 for variable i
             if (inseg) {
                 W.rt[i][q] = make_double2(rho, th);
                 W.xs[i][q] = EVAL ? iv : xv; // evaluation: 1/x_i for the diag(1/x) epilogue
@@ -1567,7 +1612,7 @@ __global__ void __launch_bounds__(GeoW<N>::SNT, GeoW<N>::SMINB) k_stepw(const De
                     double rho, th;
                     double2 iv;
                     int st = 0;
-                    log_split(xn, rho, th, iv, st);
+                    log_split_t(xn, rho, th, iv, st, S.logtab, S.atantab);
                     W.rt[col][q] = make_double2(rho, th);
                     if (st) atomicOr(&W.st[q], st);
                 }
@@ -1653,7 +1698,7 @@ __global__ void __launch_bounds__(PHT_EVALP_T, 4) k_evalp(const DevSys S, const 
                 }
             } else {
                 double2 iv;
-                log_split(v, rho, th, iv, st);
+                log_split_t(v, rho, th, iv, st, S.logtab, S.atantab);
                 sm.inv[j][tid] = iv;
             }
             sm.rt[j][tid] = make_double2(rho, th);
@@ -2257,7 +2302,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
                 }
             } else {
                 double2 iv;
-                log_split(xv, rho, th, iv, st);
+                log_split_t(xv, rho, th, iv, st, S.logtab, S.atantab);
             }
             W.rt[i][q] = make_double2(rho, th);
             if (st) atomicOr(&W.st[q], st);

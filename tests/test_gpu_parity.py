@@ -331,3 +331,26 @@ def test_row_rescale_keeps_entries_far_below_the_row(P, family):
     assert np.allclose(row(Jz[:, 0, 0]), 2.0 ** -600, rtol=1e-12, atol=0), row(Jz[:, 0, 0]) * 2.0 ** 600
     assert np.allclose(row(Jz[:, 0, 1]), 2.0, rtol=1e-12, atol=0), row(Jz[:, 0, 1])
     # (pht_evaluate's dh/dx1 = 1 is 2^-1200 of that row: below the row_exp2 representation, A25)
+
+
+@pytest.mark.parametrize("family", ["warp", "lane", "tile", "dense"])
+def test_log_split_round_trip(P, family):
+    """Stage 1 (a1) through evaluation and back: h = x (one term, exponent 1) returns
+    H = exp(log|x|) cis(arg x) = x and dh/dx = 1 for every octant, both signed zeros of the
+    imaginary part, and |x| from 1e-140 to 1e140 (the table-driven log / atan2 of the warp and lane
+    kernels, libdevice in the tile kernel).  Bound: ~2u |log|x|| from the log, ~1 ulp of pi from the
+    angle and a few ulp from exp*cis."""
+    sysm = W.from_terms("id", 1, [[((1,), 1.0, 0)]], coeffs="native")
+    g = P.System.from_workload(sysm).set_kernels(family)
+    rng = np.random.default_rng(21)
+    mag = np.exp(rng.uniform(-322, 322, 4000))
+    ang = rng.uniform(-np.pi, np.pi, 4000)
+    ang[:16] = np.arange(16) * np.pi / 8 - np.pi                 # octant boundaries
+    x = mag * np.exp(1j * ang)
+    x[16:20] = [1.0 + 0.0j, -1.0 + 0.0j, complex(-1.0, -0.0), complex(0.0, -3.0)]
+    x = x[:, None]
+    H, Jx, Jt, st = [a.cpu().numpy() for a in g.evaluate(_cuda(x), _cuda(np.ones(len(x))))]
+    assert np.all(st == 0)
+    bound = 2.2e-16 * 3 * (np.abs(np.log(np.abs(x[:, 0]))) + 8)
+    assert np.all(np.abs(H[:, 0] - x[:, 0]) / np.abs(x[:, 0]) <= bound)
+    assert np.all(np.abs(Jx[:, 0, 0] - 1.0) <= bound)
