@@ -890,18 +890,22 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
             // branch-free: pivot at or below the threshold, or too large for a normal |a_j|^2
             const double pa = cabs1(a[j]);
             singular = singular || (me && !(pa > thr && pa < 0x1p510));
-            myrcp = me ? crcp : myrcp;
         }
-        // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row (measured:
-        // predicating the elimination on !me and re-reading the pivot reciprocal from prow at the
-        // end, which saves ~80 selects, is 2% slower -- the divergent branch costs more)
+        // branch-free elimination: the pivot lane uses multiplier 0 and keeps its row; column j of
+        // the other rows is not read again, so it is not zeroed (measured: predicating the
+        // elimination on !me instead of the multiplier select is 2% slower -- divergence)
         double2 l = cmul(a[j], rcp);
         l = me ? make_double2(0.0, 0.0) : l;
 #pragma unroll
         for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, prow[c]);
-        a[j] = me ? a[j] : make_double2(0.0, 0.0);
         __syncwarp();
         }
+    }
+    if (!SHFL) {
+        // prow[c] (c < N) still holds the reciprocal of column c's pivot (later steps only write
+        // prow[j'..] with j' > c): the lane's own pivot reciprocal without a select per pivot
+        myrcp = prow[col];
+        __syncwarp(); // the caller may reuse prow
     }
     const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
     dE = make_double2(-e.x, -e.y);
