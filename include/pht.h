@@ -22,6 +22,9 @@
  *     caller; calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default
  *     stream) and never synchronise the host (except the *_host variants).
  *   - A NULL output pointer skips that output.
+ *   - Device arrays must be naturally aligned: complex (c128) arrays to 16 bytes (they are moved as
+ *     16-byte vectors; torch/cudaMalloc allocations always are), double and int64 arrays to 8,
+ *     int32 arrays to 4; otherwise PHT_EINVAL.
  *   - API misuse returns a negative pht_status synchronously; numerical conditions are
  *     reported per point in `status` (PHT_PT_* bits) and never abort the batch.
  *   - The handle is immutable after creation and may be used from several streams.

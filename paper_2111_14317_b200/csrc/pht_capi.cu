@@ -571,6 +571,11 @@ extern "C" int64_t pht_specialize_source(int32_t n_eq, int32_t n_var, const int6
 //                vs 492, katsura-10 356 vs 344 M evals/s); the specialised tile kernel below n = 10
 //                when loaded (cyclic-5 3080 vs 2760); else k_stepw (n <= 12) or k_pht
 // A forced family applies wherever it implements the entry point, AUTO elsewhere.
+// complex arrays are read and written as 16-byte vectors (double2), real arrays as doubles: a
+// misaligned pointer would fault the context, so it is refused up front (PHT_EINVAL)
+static bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+static bool al8(const void *p) { return ((uintptr_t)p & 7u) == 0; }
+
 static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *stream)
 {
     if (A0.P == 0) return PHT_OK;
@@ -653,6 +658,7 @@ extern "C" int pht_evaluate(const pht_system *s, int64_t p, const double *x, con
                             double *Jx, double *Jt, int32_t *row_exp2, uint8_t *status, void *stream)
 {
     if (!s || p < 0 || (p > 0 && (!x || !t))) return PHT_EINVAL;
+    if (!al16(x) || !al8(t) || !al16(H) || !al16(Jx) || !al16(Jt) || ((uintptr_t)row_exp2 & 3u)) return PHT_EINVAL;
     pht::Args A{};
     A.P = p;
     A.xin = (const double2 *)x;
@@ -669,6 +675,7 @@ extern "C" int pht_evaluate_log(const pht_system *s, int64_t p, const double *z,
                                 double *Jz, double *Jtau, int32_t *row_exp2, uint8_t *status, void *stream)
 {
     if (!s || p < 0 || (p > 0 && (!z || !tau))) return PHT_EINVAL;
+    if (!al16(z) || !al8(tau) || !al16(H) || !al16(Jz) || !al16(Jtau) || ((uintptr_t)row_exp2 & 3u)) return PHT_EINVAL;
     pht::Args A{};
     A.P = p;
     A.xin = (const double2 *)z;
@@ -685,6 +692,7 @@ extern "C" int pht_euler_newton(const pht_system *s, int64_t p, const double *x,
                                 double *dN, uint8_t *status, void *stream)
 {
     if (!s || p < 0 || (p > 0 && (!x || !t))) return PHT_EINVAL;
+    if (!al16(x) || !al8(t) || !al16(dE) || !al16(dN)) return PHT_EINVAL;
     pht::Args A{};
     A.P = p;
     A.xin = (const double2 *)x;
@@ -699,6 +707,7 @@ extern "C" int pht_pc_step(const pht_system *s, int64_t p, double *x, double *ta
                            int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
 {
     if (!s || p < 0 || newton_iters < 0 || (p > 0 && (!x || !tau || !dtau))) return PHT_EINVAL;
+    if (!al16(x) || !al8(tau) || !al8(dtau) || !al8(dn_norm)) return PHT_EINVAL;
     pht::Args A{};
     A.P = p;
     A.xio = (double2 *)x;
@@ -732,6 +741,7 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
 {
     pht_system *s = const_cast<pht_system *>(cs);
     if (!s || p < 0 || newton_iters < 0 || (p > 0 && (!x || !tau || !dtau))) return PHT_EINVAL;
+    if (!al8(x) || !al8(tau) || !al8(dtau) || !al8(dn_norm)) return PHT_EINVAL; // host buffers (copied)
     if (p == 0) return PHT_OK;
     std::lock_guard<std::mutex> lk(s->ws_mu);
     DevGuard g(s->device);
@@ -827,6 +837,7 @@ extern "C" int pht_homogenize(const pht_system *s, int64_t p, const double *x, i
                               void *stream)
 {
     if (!s || !s->proj || p < 0 || (p > 0 && (!x || !y))) return PHT_EINVAL;
+    if (!al16(x) || !al16(y)) return PHT_EINVAL;
     if (p == 0) return PHT_OK;
     DevGuard g(s->device);
     if (!g.ok) return cuda_fail(cudaGetLastError());
@@ -865,6 +876,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
                       void *stream)
 {
     if (!s || p < 0 || (p > 0 && (!x || !tau || !status))) return PHT_EINVAL;
+    if (!al16(x) || !al8(tau) || !al8(stats) || !al8(cellw) || ((uintptr_t)path_cell & 3u)) return PHT_EINVAL;
     if (cellw && (!path_cell || ncells < 1 || ncells > INT32_MAX || s->dropped)) return PHT_EINVAL;
     if (p == 0) return PHT_OK;
     pht_track_opts o;

@@ -354,3 +354,26 @@ def test_log_split_round_trip(P, family):
     bound = 2.2e-16 * 3 * (np.abs(np.log(np.abs(x[:, 0]))) + 8)
     assert np.all(np.abs(H[:, 0] - x[:, 0]) / np.abs(x[:, 0]) <= bound)
     assert np.all(np.abs(Jx[:, 0, 0] - 1.0) <= bound)
+
+
+def test_misaligned_complex_pointers_are_refused(P):
+    """Complex arrays move as 16-byte vectors: an only 8-byte-aligned complex pointer is refused
+    with PHT_EINVAL up front instead of faulting the context (include/pht.h conventions)."""
+    import ctypes
+    sysm = W.cyclic(10, lift_max=100)
+    g = P.System.from_workload(sysm)
+    p, n = 100, 10
+    x, t, _ = W.random_points(p, n, seed=44)
+    xd, td = _cuda(x), _cuda(t)
+    buf = torch.zeros(2 * p * n * n + 1, dtype=torch.float64, device="cuda")
+    st = torch.empty(p, dtype=torch.uint8, device="cuda")
+    cs = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    X, T, S = ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(td.data_ptr()), ctypes.c_void_p(st.data_ptr())
+    bad = ctypes.c_void_p(buf.data_ptr() + 8)
+    assert g._lib.pht_evaluate(g._h, p, X, T, None, bad, None, None, S, cs) == -1
+    assert g._lib.pht_evaluate(g._h, p, ctypes.c_void_p(buf.data_ptr() + 8), T, None, None, None, None, S, cs) == -1
+    assert g._lib.pht_euler_newton(g._h, p, X, T, bad, None, S, cs) == -1
+    # the handle and the context still work
+    H, J, Jt, st2 = g.evaluate(xd, td)
+    torch.cuda.synchronize()
+    assert bool((st2 == 0).all())
