@@ -1416,18 +1416,24 @@ __device__ __forceinline__ void pack_rec_w(const double2 *src, double2 *dst)
     }
 }
 
+// compact record (3 x 16 B, RecW<N>::C16) -> doubles
+template <int N>
+__device__ __forceinline__ void unpack_rec16(const uint4 &u0, const uint4 &u1, const uint4 &u2, double (&a)[rec_stride(N)])
+{
+    const unsigned e[6] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y};
+#pragma unroll
+    for (int j = 0; j < N && j < 12; ++j) a[j] = (double)(short)(e[j >> 1] >> (16 * (j & 1))); // I2F.F64.S16
+    a[N] = __hiloint2double((int)u1.w, (int)u1.z);
+    a[N + 1] = __hiloint2double((int)u2.y, (int)u2.x);
+    a[N + 2] = __hiloint2double((int)u2.w, (int)u2.z);
+}
+
 template <int N>
 __device__ __forceinline__ void load_rec_s(const double2 *r, double (&a)[rec_stride(N)])
 {
     if (RecW<N>::C16) {
         const uint4 *u = reinterpret_cast<const uint4 *>(r);
-        const uint4 u0 = u[0], u1 = u[1], u2 = u[2];
-        const unsigned e[6] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y};
-#pragma unroll
-        for (int j = 0; j < N && j < 12; ++j) a[j] = (double)(short)(e[j >> 1] >> (16 * (j & 1))); // I2F.F64.S16
-        a[N] = __hiloint2double((int)u1.w, (int)u1.z);
-        a[N + 1] = __hiloint2double((int)u2.y, (int)u2.x);
-        a[N + 2] = __hiloint2double((int)u2.w, (int)u2.z);
+        unpack_rec16<N>(u[0], u[1], u[2], a);
     } else {
 #pragma unroll
         for (int u = 0; u < rec_stride(N) / 2; ++u) {
