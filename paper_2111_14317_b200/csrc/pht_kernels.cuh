@@ -923,7 +923,9 @@ __device__ __forceinline__ void lsolve(Smem<N> &sm, int lane, int w, int g, int 
     const int seg = inseg ? seg0 : 0, i = inseg ? lane - seg0 * N : 0;
     q = g * PPW + seg;
     act = inseg && (q < Geo<N>::PTS);
-    const int qc = (q < Geo<N>::PTS) ? q : 0;
+    // lanes without a point of their own read their group's first point (same warp: no cross-warp
+    // access to another group's slot; compute-sanitizer racecheck)
+    const int qc = (q < Geo<N>::PTS) ? q : g * PPW;
     double2 *slot = sm.mat + qc * MS;
     unsigned *kseg = &sm.keys[w][seg * KS];
     double2 a[RW];
@@ -965,7 +967,7 @@ __device__ __forceinline__ void qsolve(Smem<N> &sm, int lane, int g, int &col, d
     q = g * PPQ + seg;
     const bool live = inseg && (q < Geo<N>::PTS);
     act = live && (c < N);
-    const int qc = live ? q : 0;
+    const int qc = live ? q : g * PPQ; // (see lsolve: same-warp slot for lanes without a point)
     double2 *slot = sm.mat + qc * MS;
     double *scr = reinterpret_cast<double *>(slot);
     double2 a[N];
