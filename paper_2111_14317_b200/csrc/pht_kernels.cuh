@@ -280,16 +280,9 @@ __device__ __forceinline__ void log_split(double2 x, double &rho, double &th, do
 // with s = 2^e m, c_j the midpoint of m's 1/128 interval, r = m / c_j - 1 (|r| <= 2^-8, degree-7
 // series); atan(t) for t = min/max in [0, 1] as atan(k/64) + atan((t - t_k) / (1 + t t_k))
 // (|u| <= 2^-7, degree-7 series), then the octant.  Extreme magnitudes take log_split.
-__device__ __forceinline__ void log_split_t(double2 x, double &rho, double &th, double2 &inv, int &st,
-                                            const double2 *logtab, const double *atantab)
+// log s for a normal s (2^-1022 < s < 2^1024), table-driven (see log_split_t)
+__device__ __forceinline__ double log_t(double s, const double2 *logtab)
 {
-    const double ax = fabs(x.x), ay = fabs(x.y);
-    const double m = fmax(ax, ay);
-    if (!(m > 0x1p-500 && m < 0x1p+500)) { // zero, non-finite or extreme: the general routine
-        log_split(x, rho, th, inv, st);
-        return;
-    }
-    const double s = fma(x.x, x.x, x.y * x.y);
     const long long bits = __double_as_longlong(s);
     const int j = (int)(bits >> 45) & 127;
     const double mm = __longlong_as_double((bits & 0x000fffffffffffffll) | 0x3ff0000000000000ll);
@@ -301,9 +294,13 @@ __device__ __forceinline__ void log_split_t(double2 x, double &rho, double &th, 
     q = fma(q, r, 1.0 / 3.0);
     q = fma(q, r, -0.5);
     const double ef = (double)((int)(bits >> 52) - 1023);
-    rho = 0.5 * fma(ef, KC[12], tj.y + fma(ef, KC[13], fma(q * r, r, r)));
-    const double is = rcp_nr(s);
-    inv = make_double2(x.x * is, -x.y * is);
+    return fma(ef, KC[12], tj.y + fma(ef, KC[13], fma(q * r, r, r)));
+}
+// atan2(y, x) for finite (x, y) not both 0 with max(|x|, |y|) normal, table-driven (see log_split_t);
+// m = max(|x|, |y|)
+__device__ __forceinline__ double atan2_t(double y, double x, double m, const double *atantab)
+{
+    const double ax = fabs(x), ay = fabs(y);
     const bool swap = ay > ax;
     const double t = (swap ? ax : ay) * rcp_nr(m);
     const double kd = rint(t * 64.0);
@@ -314,8 +311,23 @@ __device__ __forceinline__ void log_split_t(double2 x, double &rho, double &th, 
     w = fma(w, u2, -1.0 / 3.0);
     const double at = __ldg(atantab + (int)kd) + fma(w * u2, u, u);
     double a = swap ? (0x1.921fb54442d18p+0 - at) + 0x1.1a62633145c07p-54 : at; // pi/2 - at
-    a = (x.x < 0.0) ? (0x1.921fb54442d18p+1 - a) + 0x1.1a62633145c07p-53 : a;  // pi - a
-    th = (x.y < 0.0) ? -a : a;
+    a = (x < 0.0) ? (0x1.921fb54442d18p+1 - a) + 0x1.1a62633145c07p-53 : a;    // pi - a
+    return (y < 0.0) ? -a : a;
+}
+
+__device__ __forceinline__ void log_split_t(double2 x, double &rho, double &th, double2 &inv, int &st,
+                                            const double2 *logtab, const double *atantab)
+{
+    const double m = fmax(fabs(x.x), fabs(x.y));
+    if (!(m > 0x1p-500 && m < 0x1p+500)) { // zero, non-finite or extreme: the general routine
+        log_split(x, rho, th, inv, st);
+        return;
+    }
+    const double s = fma(x.x, x.x, x.y * x.y);
+    rho = 0.5 * log_t(s, logtab);
+    const double is = rcp_nr(s);
+    inv = make_double2(x.x * is, -x.y * is);
+    th = atan2_t(x.y, x.x, m, atantab);
 }
 
 // a3: w = exp(y) * (cos th + i sin th), y <= ~0.35 by construction of the row exponent.
@@ -1841,6 +1853,20 @@ __device__ __forceinline__ double2 zlog1p_add(double2 z, double2 u)
     const double im = atan2(u.y, 1.0 + u.x);
     return make_double2(z.x + re, z.y + im);
 }
+// the same with the table-driven log / atan2 (log_split_t): log|1 + u|^2 = log(s_hi) + log1p(s_lo /
+// s_hi) with s_hi + s_lo = 1 + v exactly (Fast2Sum, v = 2 Re u + |u|^2 > -1, |v| <= 1 taken here),
+// the second term to first order (|s_lo / s_hi| <= u); libdevice outside 1/4 < |1 + u| < 4 or for
+// non-finite u
+__device__ __forceinline__ double2 zlog1p_add_t(double2 z, double2 u, const double2 *logtab, const double *atantab)
+{
+    const double v = fma(u.x, 2.0 + u.x, u.y * u.y);
+    const double wx = 1.0 + u.x, m = fmax(fabs(wx), fabs(u.y));
+    if (!(fabs(v) <= 1.0 && m > 0.25 && m < 4.0)) return zlog1p_add(z, u);
+    const double sh = 1.0 + v, sl = (1.0 - sh) + v;
+    const double re = 0.5 * fma(sl, rcp_nr(sh), log_t(sh, logtab));
+    const double im = atan2_t(u.y, wx, m, atantab);
+    return make_double2(z.x + re, z.y + im);
+}
 
 // Euler predictor in the log chart: z + h delta (log state) or x exp(h delta) (x state)
 template <bool LOGS>
@@ -1854,9 +1880,9 @@ __device__ __forceinline__ double2 trk_predict_log(double2 v, double2 delta, dou
 }
 
 template <int N, bool LOGS>
-__device__ __forceinline__ double2 trk_update(double2 v, double2 delta, double h)
+__device__ __forceinline__ double2 trk_update(double2 v, double2 delta, double h, const DevSys &S)
 {
-    if (LOGS) return zlog1p_add(v, make_double2(h * delta.x, h * delta.y));
+    if (LOGS) return zlog1p_add_t(v, make_double2(h * delta.x, h * delta.y), S.logtab, S.atantab);
     const double2 d = cmul(v, delta);
     return make_double2(fma(h, d.x, v.x), fma(h, d.y, v.y));
 }
@@ -2065,18 +2091,18 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                                                    h00 * zp.y + h10 * D * ep.y + h01 * za.y + h11 * D * dl.y);
                     } else {
                         T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], dl, h)
-                                                 : trk_update<N, LOGS>(T.xa[j][qq], dl, h);
+                                                 : trk_update<N, LOGS>(T.xa[j][qq], dl, h, S);
                     }
                     T.ec[j][qq] = dl;
                 } else if (ph == PH_CORRECT) {
                     const double2 v = T.xt[j][qq];
-                    T.xt[j][qq] = trk_update<N, LOGS>(v, dl, 1.0);
+                    T.xt[j][qq] = trk_update<N, LOGS>(v, dl, 1.0, S);
                     // |dx_j / x_j|^2 (reading R14); projective: |dy_j|^2 with ||y|| = 1 (R29)
                     const double r2 = fma(dl.x, dl.x, dl.y * dl.y);
                     T.nd2[j][qq] = S.proj ? r2 * fma(v.x, v.x, v.y * v.y) : r2;
                 } else { // FINAL
                     const double2 v = T.xa[j][qq];
-                    T.xa[j][qq] = trk_update<N, LOGS>(v, dl, 1.0);
+                    T.xa[j][qq] = trk_update<N, LOGS>(v, dl, 1.0, S);
                     const double r2 = fma(dl.x, dl.x, dl.y * dl.y);
                     T.nd2[j][qq] = S.proj ? r2 * fma(v.x, v.x, v.y * v.y) : r2;
                 }
@@ -2350,14 +2376,14 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
                 if (ph == PH_PREDICT) {
                     const double hh = fmin(W.dt[q], -W.tau_a[q]);
                     W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], dl, hh)
-                                            : trk_update<N, LOGS>(W.xa[i][q], dl, hh);
+                                            : trk_update<N, LOGS>(W.xa[i][q], dl, hh, S);
                 } else if (ph == PH_CORRECT) {
                     const double2 v = W.xt[i][q];
-                    W.xt[i][q] = trk_update<N, LOGS>(v, dl, 1.0);
+                    W.xt[i][q] = trk_update<N, LOGS>(v, dl, 1.0, S);
                     W.nd2[i][q] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_i / x_i|^2 (reading R14)
                 } else { // FINAL
                     const double2 v = W.xa[i][q];
-                    W.xa[i][q] = trk_update<N, LOGS>(v, dl, 1.0);
+                    W.xa[i][q] = trk_update<N, LOGS>(v, dl, 1.0, S);
                     W.nd2[i][q] = fma(dl.x, dl.x, dl.y * dl.y);
                 }
             }
