@@ -231,7 +231,25 @@ EVAL_CONFIGS = [("cyclic-10", 1 << 21, "BASELINE.json configs[2]: cyclic-10 batc
                                           "1M evaluation points (FP64 tensor-core DMMA evaluation)")]
 
 
-def evaluation_section(world, rank, dev, reps=5):
+def evaluation_cpu_baseline(sysm, x, t, seconds=2.0):
+    """The oracle's evaluation (oracle.c orc_evaluate: repeated multiplication, symbolic
+    derivatives) on a seeded subset of the same points, all host cores; points/s."""
+    import oracle
+    o = oracle.Oracle(sysm)
+    cores = oracle.set_threads(os.cpu_count() or 1)
+    k = 256
+    t0 = time.perf_counter()
+    o.evaluate(x[:k], t[:k])
+    dt = time.perf_counter() - t0
+    k = int(min(len(x), max(k, k * seconds / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    o.evaluate(x[:k], t[:k])
+    dt = time.perf_counter() - t0
+    return {"value": k / dt, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": f"{k} points",
+            "cpu_model": cpu_model()}
+
+
+def evaluation_section(world, rank, dev, reps=5, cpu=True):
     """Standalone batched evaluation (pht_evaluate: H, Jx, Jt written to HBM) with both roofline
     fractions: HBM bytes moved (x, t in; H, Jx, Jt out) vs the measured copy bandwidth, and the
     algorithmic FP64 flops (evaluation part) vs the FP64 peak."""
@@ -287,6 +305,8 @@ def evaluation_section(world, rank, dev, reps=5):
                               "warp-per-group kernel k_stepw<N, EVAL_X>")}
         if spec_s is not None:
             out[name]["specialize_s"] = spec_s
+        if cpu and world == 1 and spec_s is None:
+            out[name]["cpu_baseline"] = evaluation_cpu_baseline(sysm, x, t)
         del g, xd, td, H, J, Jt, st
     return out
 
@@ -682,7 +702,7 @@ def main():
     tracking = tracking_section(world, rank, dev, [t for t in args.tracking.split(",") if t],
                                 fp64_peak_tflops(peak_mhz), cpu=not args.no_cpu_baseline) \
         if args.tracking else {}
-    evaluation = evaluation_section(world, rank, dev) if args.evaluation else {}
+    evaluation = evaluation_section(world, rank, dev, cpu=not args.no_cpu_baseline) if args.evaluation else {}
     paper = paper_protocol_section(dev) if (args.paper_protocol and rank == 0) else {}
 
     if rank == 0:

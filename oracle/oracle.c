@@ -626,11 +626,18 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
             continue;
         }
+        int tok = 0; /* dE holds the Euler direction of the current accepted point */
         while (tq < 0.0) {
             if (steps == max_steps) { st = ORC_PT_MAX_STEPS; break; }
             double h = fmin(dt, -tq);
-            int s1 = solve_point(&s, xq, exp(tq), dE, 0);
-            ++evals;
+            /* after a rejection the predictor restarts from the same point: its Euler direction is
+             * the one already computed (the same evaluation; not repeated) */
+            int s1 = 0;
+            if (!tok) {
+                s1 = solve_point(&s, xq, exp(tq), dE, 0);
+                ++evals;
+                tok = !s1;
+            }
             int ok = 0;
             double tt = tq + h;
             if (!s1) {
@@ -661,6 +668,7 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             }
             if (ok) {
                 memcpy(xq, xt, sizeof(double) * 2 * n);
+                tok = 0;
                 tq = tt;
                 ++steps;
                 if (pred_tol > 0.0) { /* next step from the Euler predictor's error e1 = O(dt^2) */
@@ -815,11 +823,16 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
             for (int u = 0; u < 4; ++u) stats[4 * q + u] = 0;
             continue;
         }
+        int tok = 0; /* dE holds the Euler direction of the current accepted point (as orc_track) */
         while (tq < 0.0) {
             if (steps == max_steps) { st = ORC_PT_MAX_STEPS; break; }
             double h = fmin(dt, -tq);
-            int s1 = solve_point_x(&s, xq, tq, wr, dE, 0);
-            ++evals;
+            int s1 = 0;
+            if (!tok || hermite) { /* (the Hermite predictor keeps the round-1 evaluation count) */
+                s1 = solve_point_x(&s, xq, tq, wr, dE, 0);
+                ++evals;
+                tok = !s1;
+            }
             int ok = 0;
             double tt = tq + h;
             if (!s1) {
@@ -866,6 +879,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                     for (int j = 0; j < n; ++j) { zp[j] = zq[j]; ep[j] = load(dE + 2 * j); }
                 has_prev = 1;
                 tp = tq;
+                tok = 0;
                 for (int j = 0; j < n; ++j) { xq[j] = xt[j]; zq[j] = zt[j]; }
                 tq = tt;
                 ++steps;

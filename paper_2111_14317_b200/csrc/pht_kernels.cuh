@@ -1787,6 +1787,8 @@ struct TrackSmem {
     double nd2[N][Geo<N>::WL + 1];   // |dx_j / x_j|^2 of this iteration
     double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL], nd1[Geo<N>::WL], tau_p[Geo<N>::WL];
     int has_prev[Geo<N>::WL];
+    int tok[Geo<N>::WL];    // the Euler direction of the accepted point is in ec (its evaluation succeeded)
+    int repred[Geo<N>::WL]; // next iteration: form the trial point from ec without an evaluation
     long long path[Geo<N>::WL], steps[Geo<N>::WL], rej[Geo<N>::WL], evals[Geo<N>::WL], fin[Geo<N>::WL];
     int phase[Geo<N>::WL], it[Geo<N>::WL], succ[Geo<N>::WL], cell[Geo<N>::WL];
     int acc[Geo<N>::WL];         // this iteration: 1 accept x~ -> x
@@ -1823,6 +1825,8 @@ __device__ __forceinline__ void trk_pop(TT &T, const TrackArgs &A, int q)
         T.succ[q] = 0;
         T.it[q] = 0;
         T.has_prev[q] = 0;
+        T.tok[q] = 0;
+        T.repred[q] = 0;
         T.phase[q] = (t0 < 0.0) ? PH_PREDICT : PH_FINAL;
     } else {
         T.path[q] = -1;
@@ -1904,6 +1908,7 @@ __device__ __forceinline__ void trk_decide(TT &T, const TrackArgs &A, const DevS
             T.phase[qq] = PH_CORRECT;
             T.it[qq] = 1;
             T.prev[qq] = INFINITY;
+            T.tok[qq] = 1; // this evaluation's Euler direction (at the accepted point) is in ec
         }
     } else if (ph == PH_CORRECT) {
         if (bad) reject = true;
@@ -1916,6 +1921,7 @@ __device__ __forceinline__ void trk_decide(TT &T, const TrackArgs &A, const DevS
             // quadratic-convergence estimate of the remaining error), <= newton_tol (R14)
             if (nd <= o.newton_tol || (T.it[qq] >= 2 && nd * (nd / T.prev[qq]) <= o.newton_tol)) {
                 T.acc[qq] = 1;
+                T.tok[qq] = 0; // the accepted point moves: its Euler direction is not known yet
                 T.tau_p[qq] = T.tau_a[qq];
                 T.has_prev[qq] = 1;
                 T.tau_a[qq] = T.tau_t[qq];
@@ -1965,6 +1971,16 @@ __device__ __forceinline__ void trk_decide(TT &T, const TrackArgs &A, const DevS
         else {
             T.phase[qq] = PH_PREDICT;
             if (T.steps[qq] == o.max_steps) finish = 16;
+            else if (ph == PH_CORRECT && T.tok[qq] && o.predictor != 1 && !S.proj) {
+                // re-prediction from the same accepted point: its Euler direction is the cached one
+                // (bitwise the evaluation the PREDICT phase would repeat), so the trial point is
+                // formed without an evaluation and the next evaluation is the first correction
+                T.tau_t[qq] = T.tau_a[qq] + fmin(T.dt[qq], -T.tau_a[qq]);
+                T.phase[qq] = PH_CORRECT;
+                T.it[qq] = 1;
+                T.prev[qq] = INFINITY;
+                T.repred[qq] = 1;
+            }
         }
     }
     if (finish >= 0) {
@@ -2007,6 +2023,11 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             }
             if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
             if (T.refill[qq]) T.xa[j][qq] = A.x[T.path[qq] * N + j];
+            if (T.repred[qq]) { // re-prediction from the cached Euler direction (trk_decide)
+                const double h = fmin(T.dt[qq], -T.tau_a[qq]);
+                T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], T.ec[j][qq], h)
+                                         : trk_update<N, LOGS>(T.xa[j][qq], T.ec[j][qq], h, S);
+            }
             const int ph = T.phase[qq];
             sm.xs[j][qq] = (ph == PH_CORRECT) ? T.xt[j][qq]
                                               : (ph == PH_IDLE ? make_double2(LOGS ? 0.0 : 1.0, 0.0) : T.xa[j][qq]);
@@ -2020,6 +2041,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             T.done_path[tid] = -1;
             T.acc[tid] = 0;
             T.refill[tid] = 0;
+            if (tid < PTS) T.repred[tid] = 0;
             sm.st[tid] = 0;
             const int ph = (tid < PTS) ? T.phase[tid] : PH_IDLE;
             sm.tau[tid] = (ph == PH_CORRECT) ? T.tau_t[tid] : ((ph == PH_PREDICT) ? T.tau_a[tid] : 0.0);
@@ -2165,6 +2187,7 @@ struct TrackW {
     double2 rt[N][PPW];                 // (rho, vartheta) of the query points
     double2 xa[N][PPW], xt[N][PPW];     // accepted and trial points
     double2 dd[N][PPW];                 // direction of this iteration
+    double2 ec[N][PPW];                 // Euler direction at the accepted point (re-prediction)
     double nd2[N][PPW];
     double2 prow[PPW][GeoW<N>::RW | 1];
     alignas(16) unsigned keys[PPW * GeoW<N>::KS];
@@ -2172,6 +2195,7 @@ struct TrackW {
     double tau_a[PPW], tau_t[PPW], dt[PPW], prev[PPW], nd1[PPW], tau_p[PPW];
     long long path[PPW], steps[PPW], rej[PPW], evals[PPW], fin[PPW], done_path[PPW];
     int phase[PPW], it[PPW], succ[PPW], cell[PPW], acc[PPW], refill[PPW], has_prev[PPW], st[PPW];
+    int tok[PPW], repred[PPW];          // (see TrackSmem)
 };
 
 template <int N, int LPR = 1>
@@ -2313,6 +2337,11 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             if (W.acc[q]) W.xa[i][q] = W.xt[i][q];
             if (W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
             if (W.refill[q]) W.xa[i][q] = A.x[W.path[q] * N + i];
+            if (W.repred[q]) { // re-prediction from the cached Euler direction (trk_decide)
+                const double hh = fmin(W.dt[q], -W.tau_a[q]);
+                W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], W.ec[i][q], hh)
+                                        : trk_update<N, LOGS>(W.xa[i][q], W.ec[i][q], hh, S);
+            }
             const int ph = W.phase[q];
             if (ph == PH_CORRECT) xv = W.xt[i][q];
             else if (ph != PH_IDLE) xv = W.xa[i][q];
@@ -2322,6 +2351,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             W.done_path[lane] = -1;
             W.acc[lane] = 0;
             W.refill[lane] = 0;
+            W.repred[lane] = 0;
             W.st[lane] = 0;
             const int ph = W.phase[lane];
             W.tau[lane] = (ph == PH_CORRECT) ? W.tau_t[lane] : ((ph == PH_PREDICT) ? W.tau_a[lane] : 0.0);
@@ -2375,6 +2405,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
                 const double2 dl = W.dd[i][q];
                 if (ph == PH_PREDICT) {
                     const double hh = fmin(W.dt[q], -W.tau_a[q]);
+                    W.ec[i][q] = dl; // cached for a re-prediction after a rejection
                     W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], dl, hh)
                                             : trk_update<N, LOGS>(W.xa[i][q], dl, hh, S);
                 } else if (ph == PH_CORRECT) {
