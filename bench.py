@@ -509,6 +509,32 @@ def tracking_section(world, rank, dev, which, peak_tflops, cpu=True):
                 cb = tracking_cpu_baseline(sysm, w0, tau0, cid, Wc)
                 cb["gpu_over_cpu_paths_per_s"] = out[name]["paths_per_s"] / cb["all_cores"]["paths_per_s"]
                 out[name]["cpu_baseline"] = cb
+        # the consolidation's payoff as an option (pht_track_opts.reuse_tangent): the last
+        # corrector solve's Euler direction predicts the next step; same single gather
+        runs_r = []
+        for r in range(TRACK_REPS):
+            zr2, tr2 = zl.clone(), tl.clone()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st2, stats2 = g.track_cells(zr2, tr2, wcell, cl, reuse_tangent=1)
+            res2 = gather_to_rank0({"z": zr2, "status": st2, "stats": stats2}, idx, Ptot) if world > 1 else \
+                {"z": zr2, "status": st2, "stats": stats2}
+            e2.record()
+            torch.cuda.synchronize(dev)
+            ms2 = torch.tensor([e0.elapsed_time(e2)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+            runs_r.append(float(ms2.item()))
+        if rank == 0:
+            sv2, ss2 = res2["status"].cpu().numpy(), res2["stats"].cpu().numpy()
+            t2 = float(np.median(runs_r))
+            out[name]["reuse_tangent"] = {
+                "ms": t2, "paths_per_s": Ptot / (t2 * 1e-3), "evals": int(ss2[:, 2].sum()),
+                "finite": int(((sv2 == 0) | (sv2 == 64)).sum()), "runs_ms": runs_r,
+                "option": "pht_track_opts.reuse_tangent = 1 (oracle parity: tests/test_gpu_track.py)"}
         if name == "cyclic-10":
             for proj in (False, True):
                 r2 = _second_stage(world, rank, dev, sysm, L, zr, st, proj)   # from this rank's endpoints
@@ -744,6 +770,8 @@ def main():
         line["summary"] = {
             "step_evals_per_s": value, "step_frac": achieved / peak, "e2e_evals_per_s": e2e_value,
             "paths_per_s": {k: v.get("paths_per_s") for k, v in tracking.items()},
+            "paths_per_s_reuse_tangent": {k: v["reuse_tangent"]["paths_per_s"] for k, v in tracking.items()
+                                          if "reuse_tangent" in v},
             "tracking_ms": {k: v.get("ms") for k, v in tracking.items()},
             "tracking_frac": {k: v["roofline"]["frac"] for k, v in tracking.items() if "roofline" in v},
             "tracking_finite": {k: v.get("finite", v.get("status", {}).get("finite")) for k, v in tracking.items()},

@@ -327,6 +327,11 @@ typedef struct {
                              extrapolation in the log chart through the previous and the current
                              accepted point and their Euler directions (log chart
                              only, i.e. pred_log = 1: Euler otherwise)                        */
+    int32_t reuse_tangent; /* 0 (default); 1: the consolidated solve of the last corrector iteration
+                             also yields the Euler direction at that iterate; it
+                             serves as the next step's predictor direction, one evaluation fewer
+                             per accepted step (first-order different from the tangent at the
+                             accepted point; Euler predictor, affine systems)                    */
 } pht_track_opts;
 
 void pht_track_opts_default(pht_track_opts *opts);
@@ -360,7 +365,7 @@ const char *pht_strerror(int code);
 const char *pht_last_cuda_error(void);
 
 /* ABI version (incremented on any signature change). */
-int pht_version(void); /* 2: pht_system_set_kernels, PHT_PT_FLOOR */
+int pht_version(void); /* 3: pht_track_opts.reuse_tangent; 2: pht_system_set_kernels, PHT_PT_FLOOR */
 
 #ifdef __cplusplus
 }

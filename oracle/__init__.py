@@ -136,12 +136,12 @@ class Oracle:
 
     def track(self, x, tau, *, dtau_init=0.05, dtau_min=1e-12, dtau_max=0.5, newton_tol=1e-10,
               shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
-              max_steps=10000, final_iters=5, pred_log=0, pred_tol=0.0):
+              max_steps=10000, final_iters=5, pred_log=0, pred_tol=0.0, reuse_tangent=0):
         x = _c2(x).copy()
         tau = np.ascontiguousarray(tau, np.float64).copy()
         p = x.shape[0]
         opt = np.array([dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm, pred_tol])
-        iopt = np.array([K, grow_after, max_steps, final_iters, pred_log], np.int32)
+        iopt = np.array([K, grow_after, max_steps, final_iters, pred_log, reuse_tangent], np.int32)
         st = np.zeros(p, np.uint8)
         stats = np.zeros((p, 4), np.int64)
         rc = lib().orc_track(*self._sys_args(), ctypes.c_int64(p), _p(x), _p(tau), _p(opt), _p(iopt),
@@ -153,7 +153,7 @@ class Oracle:
     def track_x(self, xm, xe, tau, *, dtau_init=0.05, dtau_min=1e-12, dtau_max=0.5, newton_tol=1e-10,
                 shrink=0.5, grow=2.0, final_tol=1e-13, inf_norm=1e8, K=4, grow_after=3,
                 max_steps=10000, final_iters=5, pred_log=1, cell_lift=None, path_cell=None, pred_tol=0.0,
-                predictor=0):
+                predictor=0, reuse_tangent=0):
         """orc_track_x: the tracker with extended-range state x = xm * 2**xe; with cell_lift
         [ncells, M] / path_cell [p] it tracks in cell coordinates (pht_track_cells)."""
         xm = _c2(xm).copy()
@@ -161,7 +161,7 @@ class Oracle:
         tau = np.ascontiguousarray(tau, np.float64).copy()
         p = xm.shape[0]
         opt = np.array([dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm, pred_tol])
-        iopt = np.array([K, grow_after, max_steps, final_iters, pred_log, predictor], np.int32)
+        iopt = np.array([K, grow_after, max_steps, final_iters, pred_log, predictor, reuse_tangent], np.int32)
         st = np.zeros(p, np.uint8)
         stats = np.zeros((p, 4), np.int64)
         cw = None if cell_lift is None else np.ascontiguousarray(cell_lift, np.float64)

@@ -598,8 +598,10 @@ static double relmax(int n, const double *d, const double *x)
  * corrector converges when max_j |dN_j|/|x_j| <= newton_tol, a scale-invariant test because
  * polyhedral start points span many orders of magnitude).
  * opt[] = {dtau_init, dtau_min, dtau_max, newton_tol, shrink, grow, final_tol, inf_norm, pred_tol}
- * iopt[] = {K (max corrector iters), grow_after, max_steps, final_iters, pred_log}
+ * iopt[] = {K (max corrector iters), grow_after, max_steps, final_iters, pred_log, reuse_tangent}
  * pred_log: the Euler predictor in the log chart, x exp(h dz/dtau), instead of x + h dx/dtau.
+ * reuse_tangent: the last corrector solve's Euler direction (relative, dz/dtau at that iterate)
+ * predicts the next step (P:659-667 consolidation), one solve fewer per accepted step.
  * stats[q] = {accepted steps, rejected steps, evaluations (solves), final Newton iters}.
  */
 int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, const int64_t *w,
@@ -613,10 +615,10 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
     const double pred_tol = opt[8]; /* step control (reading R14), <= 0: grow_after rule */
     const int K = iopt[0], grow_after = iopt[1], max_steps = iopt[2], final_iters = iopt[3];
     if (final_iters < 1) return -1; /* as pht_track: at least one refinement iteration */
-    const int pred_log = iopt[4];
+    const int pred_log = iopt[4], reuse = iopt[5];
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
-        double *xq = x + 2 * n * q, dE[128], dN[128], xt[128];
+        double *xq = x + 2 * n * q, dE[128], dN[128], xt[128], dEn[128], rel[128];
         double tq = tau[q], dt = dtau_init;
         int64_t steps = 0, rejects = 0, evals = 0, fin = 0;
         int succ = 0, st = 0;
@@ -653,9 +655,11 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
                     for (int i = 0; i < 2 * n; ++i) xt[i] = xq[i] + h * t * dE[i];
                 }
                 for (int it = 1; it <= K; ++it) {
-                    s1 = solve_point(&s, xt, exp(tt), 0, dN);
+                    s1 = solve_point(&s, xt, exp(tt), reuse ? dEn : 0, dN);
                     ++evals;
                     if (s1) break;
+                    if (reuse) /* dz/dtau / t at this iterate (relative direction) */
+                        for (int j = 0; j < n; ++j) store(rel + 2 * j, cdiv(load(dEn + 2 * j), load(xt + 2 * j)));
                     double nd = relmax(n, dN, xt);
                     for (int i = 0; i < 2 * n; ++i) xt[i] += dN[i];
                     if (it == 1) nd1 = nd;
@@ -669,6 +673,10 @@ int orc_track(int n, const int64_t *off, const int32_t *a, const double *c, cons
             if (ok) {
                 memcpy(xq, xt, sizeof(double) * 2 * n);
                 tok = 0;
+                if (reuse && tt < 0.0) { /* the iterate's relative direction, at the accepted point */
+                    for (int j = 0; j < n; ++j) store(dE + 2 * j, cmul(load(rel + 2 * j), load(xq + 2 * j)));
+                    tok = 1;
+                }
                 tq = tt;
                 ++steps;
                 if (pred_tol > 0.0) { /* next step from the Euler predictor's error e1 = O(dt^2) */
@@ -800,10 +808,11 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
     /* predictor 1: cubic Hermite extrapolation in the log chart through the previous and the
      * current accepted point and their Euler directions, log chart only */
     const int hermite = pred_log && iopt[5] == 1;
+    const int reuse = iopt[6] && !hermite; /* reuse_tangent (see orc_track) */
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t q = 0; q < p; ++q) {
         xc xq[64], xt[64];
-        double dE[128], dN[128];
+        double dE[128], dN[128], dEn[128];
         /* continuous log coordinates of the current, trial and previous accepted points (the
          * Hermite predictor needs differences of z without branch jumps) */
         cplx zq[64], zt[64], zp[64], ep[64];
@@ -859,7 +868,7 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                     xupdate(n, xt, dE, h);
                 }
                 for (int it = 1; it <= K; ++it) {
-                    s1 = solve_point_x(&s, xt, tt, wr, 0, dN);
+                    s1 = solve_point_x(&s, xt, tt, wr, reuse ? dEn : 0, dN);
                     ++evals;
                     if (s1) break;
                     double nd = relmax_d(n, dN);
@@ -880,6 +889,10 @@ int orc_track_x(int n, const int64_t *off, const int32_t *a, const double *c, co
                 has_prev = 1;
                 tp = tq;
                 tok = 0;
+                if (reuse && tt < 0.0) { /* delta_E of the last corrector iterate (relative) */
+                    memcpy(dE, dEn, sizeof(double) * 2 * n);
+                    tok = 1;
+                }
                 for (int j = 0; j < n; ++j) { xq[j] = xt[j]; zq[j] = zt[j]; }
                 tq = tt;
                 ++steps;

@@ -61,7 +61,7 @@ class TrackOpts(ctypes.Structure):
                 ("final_tol", ctypes.c_double), ("inf_norm", ctypes.c_double), ("newton_iters", ctypes.c_int32),
                 ("grow_after", ctypes.c_int32), ("max_steps", ctypes.c_int32), ("final_iters", ctypes.c_int32),
                 ("log_state", ctypes.c_int32), ("pred_log", ctypes.c_int32), ("pred_tol", ctypes.c_double),
-                ("predictor", ctypes.c_int32)]
+                ("predictor", ctypes.c_int32), ("reuse_tangent", ctypes.c_int32)]
 
 
 class PhtError(RuntimeError):

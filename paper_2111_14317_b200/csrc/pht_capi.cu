@@ -869,6 +869,7 @@ extern "C" void pht_track_opts_default(pht_track_opts *o)
     o->pred_log = -1;
     o->predictor = 0;
     o->pred_tol = 0.0; // classic grow_after rule (measured best, profiles/r01_tracker_control.txt)
+    o->reuse_tangent = 0;
 }
 
 static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, const double *cellw, int64_t ncells,
@@ -910,7 +911,7 @@ static int track_impl(const pht_system *s, int64_t p, double *x, double *tau, co
     A.solver = s->solver;
     A.o = pht::TrackOpts{o.dtau_init, o.dtau_min, o.dtau_max, o.newton_tol, o.shrink, o.grow, o.final_tol,
                          o.inf_norm, o.newton_iters, o.grow_after, o.max_steps, o.final_iters, o.log_state,
-                         o.pred_log < 0 ? o.log_state : o.pred_log, o.pred_tol, o.predictor};
+                         o.pred_log < 0 ? o.log_state : o.pred_log, o.pred_tol, o.predictor, o.reuse_tangent};
     // AUTO: the warp-per-group tracker (k_trackw: n <= 12, LU, affine, Euler predictor) is faster
     // than the specialised tile tracker, which serves only where k_trackw does not apply and the
     // batch fills at least one wave of its (2-3x larger) tiles (measured: 70 paths 4x slower)
@@ -974,4 +975,4 @@ extern "C" const char *pht_strerror(int code)
     }
 }
 
-extern "C" int pht_version(void) { return 2; }
+extern "C" int pht_version(void) { return 3; }

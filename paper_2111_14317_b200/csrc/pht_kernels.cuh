@@ -90,6 +90,7 @@ struct TrackOpts {
     int pred_log;  // Euler predictor in the log chart: z + h dz/dtau (x exp(h dz/dtau))
     double pred_tol; // step control from the first corrector update (<= 0: grow_after rule)
     int predictor;   // 1: cubic Hermite extrapolation in the log chart (pred_log), else Euler
+    int reuse_tangent; // the last corrector iterate's Euler direction predicts the next step
 };
 struct TrackArgs {
     int64_t P;
@@ -1784,6 +1785,7 @@ struct TrackSmem {
     double2 zp[N][Geo<N>::WL + 1];   // Hermite predictor: previous accepted point (log chart) ...
     double2 ep[N][Geo<N>::WL + 1];   // ... and its Euler direction dz/dtau
     double2 ec[N][Geo<N>::WL + 1];   // Euler direction at the current accepted point
+    double2 ecn[N][Geo<N>::WL + 1];  // reuse_tangent: Euler direction at the latest corrector iterate
     double nd2[N][Geo<N>::WL + 1];   // |dx_j / x_j|^2 of this iteration
     double tau_a[Geo<N>::WL], tau_t[Geo<N>::WL], dt[Geo<N>::WL], prev[Geo<N>::WL], nd1[Geo<N>::WL], tau_p[Geo<N>::WL];
     int has_prev[Geo<N>::WL];
@@ -1936,6 +1938,16 @@ __device__ __forceinline__ void trk_decide(TT &T, const TrackArgs &A, const DevS
                 }
                 T.phase[qq] = (T.tau_a[qq] < 0.0) ? PH_PREDICT : PH_FINAL;
                 if (T.phase[qq] == PH_PREDICT && T.steps[qq] == o.max_steps) finish = 16; // MAX_STEPS
+                else if (T.phase[qq] == PH_PREDICT && o.reuse_tangent && o.predictor != 1 && !S.proj) {
+                    // reuse_tangent: the consolidated solve of the last corrector iteration gave the
+                    // Euler direction at that iterate; it predicts the next step
+                    T.tok[qq] = 1;
+                    T.tau_t[qq] = T.tau_a[qq] + fmin(T.dt[qq], -T.tau_a[qq]);
+                    T.phase[qq] = PH_CORRECT;
+                    T.it[qq] = 1;
+                    T.prev[qq] = INFINITY;
+                    T.repred[qq] = 2;
+                }
             } else if ((T.it[qq] >= 2 && nd > 0.5 * T.prev[qq]) || T.it[qq] >= o.K) {
                 reject = true;
             } else {
@@ -2024,6 +2036,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             if (T.done_path[qq] >= 0) A.x[T.done_path[qq] * N + j] = T.xa[j][qq];
             if (T.refill[qq]) T.xa[j][qq] = A.x[T.path[qq] * N + j];
             if (T.repred[qq]) { // re-prediction from the cached Euler direction (trk_decide)
+                if (T.repred[qq] == 2) T.ec[j][qq] = T.ecn[j][qq]; // reuse_tangent: the iterate's
                 const double h = fmin(T.dt[qq], -T.tau_a[qq]);
                 T.xt[j][qq] = o.pred_log ? trk_predict_log<LOGS>(T.xa[j][qq], T.ec[j][qq], h)
                                          : trk_update<N, LOGS>(T.xa[j][qq], T.ec[j][qq], h, S);
@@ -2080,6 +2093,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 if (act) {
                     if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
                     T.dd[col][qq] = (T.phase[qq] == PH_PREDICT) ? dE : dN;
+                    if (o.reuse_tangent && T.phase[qq] == PH_CORRECT) T.ecn[col][qq] = dE;
                 }
             }
         } else {
@@ -2091,6 +2105,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
                 if (act) {
                     if (sing) atomicOr(&sm.st[qq], PT_SINGULAR);
                     T.dd[col][qq] = (T.phase[qq] == PH_PREDICT) ? dE : dN;
+                    if (o.reuse_tangent && T.phase[qq] == PH_CORRECT) T.ecn[col][qq] = dE;
                 }
             }
         }
@@ -2188,6 +2203,7 @@ struct TrackW {
     double2 xa[N][PPW], xt[N][PPW];     // accepted and trial points
     double2 dd[N][PPW];                 // direction of this iteration
     double2 ec[N][PPW];                 // Euler direction at the accepted point (re-prediction)
+    double2 ecn[N][PPW];                // reuse_tangent: Euler direction at the latest corrector iterate
     double nd2[N][PPW];
     double2 prow[PPW][GeoW<N>::RW | 1];
     alignas(16) unsigned keys[PPW * GeoW<N>::KS];
@@ -2338,6 +2354,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             if (W.done_path[q] >= 0) A.x[W.done_path[q] * N + i] = W.xa[i][q];
             if (W.refill[q]) W.xa[i][q] = A.x[W.path[q] * N + i];
             if (W.repred[q]) { // re-prediction from the cached Euler direction (trk_decide)
+                if (W.repred[q] == 2) W.ec[i][q] = W.ecn[i][q]; // reuse_tangent: the iterate's
                 const double hh = fmin(W.dt[q], -W.tau_a[q]);
                 W.xt[i][q] = o.pred_log ? trk_predict_log<LOGS>(W.xa[i][q], W.ec[i][q], hh)
                                         : trk_update<N, LOGS>(W.xa[i][q], W.ec[i][q], hh, S);
@@ -2395,6 +2412,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             if (prim) {
                 if (sing) atomicOr(&W.st[q], PT_SINGULAR);
                 W.dd[col][q] = (W.phase[q] == PH_PREDICT) ? dE : dN;
+                if (o.reuse_tangent && W.phase[q] == PH_CORRECT) W.ecn[col][q] = dE;
             }
         }
         __syncwarp();
