@@ -96,8 +96,9 @@ struct pht_system {
     // dense FP64 tensor-core path (pht_dense.cuh), built when the system is genuinely dense
     int dense = 0;
     double *d_b2phi = nullptr, *d_b2th = nullptr, *d_b4 = nullptr;
-    int *d_ntoff = nullptr;
-    int max_ntk = 0; // most n-tiles (8 terms) of one equation: size of the staged B tiles
+    int *d_tinfo = nullptr; // per n-tile equation / boundary info (build_dense)
+    int max_ntk = 0; // tiles per staged chunk of B operands (most n-tiles of one equation)
+    int dense_ntiles = 0; // n-tiles of the packed term stream
     // packed tables on the host (input of the code generator, pht_system_specialize)
     std::vector<double> h_rec;
     std::vector<int> h_off;
@@ -209,9 +210,14 @@ static int pack_system(int32_t n_eq, int32_t n_var, const int64_t *off, const in
 }
 
 // FP64 tensor-core tables (pht_dense.cuh) from the packed records [a, omega, log|c|, arg c]:
-// B operands pre-swizzled into mma.m8n8k4 fragment order, one segment of n-tiles (8 terms) per
-// equation.  Stage 2: B = [A; omega; log|c|] (phi) and [A; 0; arg c] (theta), K = n + 2 padded
-// to 4; stage 4: B = [A_k | omega | 1] per 4-term half tile.
+// B operands pre-swizzled into mma.m8n8k4 fragment order.  Stage 2: B = [A; omega; log|c|] (phi)
+// and [A; 0; arg c] (theta), K = n + 2 padded to 4; stage 4: B = [A_k | omega | 1] per 4-term
+// half tile.  The terms of all equations form ONE stream cut into n-tiles of 8 slots: a tile may
+// hold the end of one equation and the start of the next (at most one equation starts inside a
+// tile; a second one is moved to the next tile, the skipped slots padded).  Per-equation tiles
+// left the last tile of every 50-term equation 2/8 used (C4: 140 tiles for 1,000 terms; packed:
+// 125).  Equation k processes the tiles that start with its terms and the boundary tile where it
+// ends (tinfo, see pht_dense.cuh).
 static int build_dense(pht_system *s)
 {
     if (s->dense) return PHT_OK;
@@ -219,48 +225,87 @@ static int build_dense(pht_system *s)
     const std::vector<double> &rec = s->h_rec;
     const std::vector<int> &off = s->h_off;
     const int KP = (n + 2 + 3) & ~3, KS = KP / 4, CT = (n + 2 + 7) / 8;
-    std::vector<int> ntoff(n + 1, 0);
+    // slot stream: global term index per slot, -1 = padding
+    std::vector<int64_t> slot;
+    std::vector<int> slot_eq;
     int max_ntk = 0;
+    bool mid_start = false; // an equation already started inside the current tile
     for (int k = 0; k < n; ++k) {
-        ntoff[k + 1] = ntoff[k] + (off[k + 1] - off[k] + 7) / 8;
-        max_ntk = std::max(max_ntk, ntoff[k + 1] - ntoff[k]);
+        const int m = off[k + 1] - off[k];
+        if (m == 0) return PHT_EINVAL;
+        max_ntk = std::max(max_ntk, (m + 7) / 8);
+        if (slot.size() % 8 != 0 && mid_start) // a second boundary in this tile: pad to the next tile
+            while (slot.size() % 8 != 0) { slot.push_back(-1); slot_eq.push_back(k - 1); }
+        mid_start = slot.size() % 8 != 0;
+        for (int t = 0; t < m; ++t) {
+            if (t > 0 && slot.size() % 8 == 0) mid_start = false; // crossed into a new tile
+            slot.push_back(off[k] + t);
+            slot_eq.push_back(k);
+        }
     }
-    const int NT = ntoff[n];
-    std::vector<double> b2p((size_t)NT * KS * 32), b2t((size_t)NT * KS * 32), b4((size_t)2 * NT * CT * 32);
+    while (slot.size() % 8 != 0) { slot.push_back(-1); slot_eq.push_back(n - 1); }
+    const int NT = (int)(slot.size() / 8);
+    // per equation k: the tiles [ts, te) it processes (those starting with its terms, plus the
+    // boundary tile where it ends and k + 1 starts); sb = that tile's first slot of k + 1 (8: no
+    // boundary tile); done: k lies entirely inside the previous boundary tile; endB: k + 1 ends
+    // inside this equation's boundary tile
+    std::vector<int> first(n, -1), last(n, -1);
+    for (size_t u = 0; u < slot.size(); ++u) {
+        if (slot[u] < 0) continue;
+        const int k = slot_eq[u];
+        if (first[k] < 0) first[k] = (int)u;
+        last[k] = (int)u;
+    }
+    std::vector<int> tinfo(2 * n);
+    max_ntk = 1;
     for (int k = 0; k < n; ++k) {
-        for (int t = 0; t < ntoff[k + 1] - ntoff[k]; ++t) {
-            const int ntg = ntoff[k] + t;
-            for (int lane = 0; lane < 32; ++lane) {
-                const int g = lane >> 2, r = lane & 3;
-                const int64_t i = off[k] + 8 * t + g; // stage 2: B[r][g] = term 8t+g
-                const bool real = i < off[k + 1];
-                const double *ri = rec.data() + (size_t)i * RS;
-                for (int kk = 0; kk < KS; ++kk) {
-                    const int kr = 4 * kk + r;
-                    double vp = 0.0, vt = 0.0;
-                    if (real) {
-                        if (kr < n) vp = vt = ri[kr];
-                        else if (kr == n) vp = ri[n];
-                        else if (kr == n + 1) { vp = ri[n + 1]; vt = ri[n + 2]; }
-                    } else if (kr == n + 1) {
-                        vp = -1e300; // padding term: exp -> 0
-                    }
-                    b2p[((size_t)ntg * KS + kk) * 32 + lane] = vp;
-                    b2t[((size_t)ntg * KS + kk) * 32 + lane] = vt;
+        const int ts = first[k] / 8 + (first[k] % 8 != 0 ? 1 : 0);
+        const int tl = last[k] / 8;
+        const bool done = ts > tl;
+        int te = done ? ts : tl + 1, sb = 8;
+        bool endB = false;
+        if (!done && k + 1 < n && first[k + 1] / 8 == tl) { // k + 1 starts inside k's last tile
+            sb = first[k + 1] % 8;
+            endB = last[k + 1] / 8 == tl;
+        }
+        if (done) te = ts;
+        max_ntk = std::max(max_ntk, te - ts);
+        if (te > 0xffff) return PHT_EUNSUPPORTED;
+        tinfo[2 * k] = ts | (te << 16);
+        tinfo[2 * k + 1] = sb | ((int)done << 8) | ((int)endB << 9);
+    }
+    std::vector<double> b2p((size_t)NT * KS * 32), b2t((size_t)NT * KS * 32), b4((size_t)2 * NT * CT * 32);
+    for (int ntg = 0; ntg < NT; ++ntg) {
+        for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane >> 2, r = lane & 3;
+            const int64_t i = slot[8 * ntg + g]; // stage 2: B[r][g] = slot 8t+g
+            const bool real = i >= 0;
+            const double *ri = rec.data() + (size_t)(real ? i : 0) * RS;
+            for (int kk = 0; kk < KS; ++kk) {
+                const int kr = 4 * kk + r;
+                double vp = 0.0, vt = 0.0;
+                if (real) {
+                    if (kr < n) vp = vt = ri[kr];
+                    else if (kr == n) vp = ri[n];
+                    else if (kr == n + 1) { vp = ri[n + 1]; vt = ri[n + 2]; }
+                } else if (kr == n + 1) {
+                    vp = -1e300; // padding slot: exp -> 0
                 }
-                for (int h = 0; h < 2; ++h) { // stage 4: B[r][g] = term 8t+4h+r, column 8ct+g
-                    const int64_t i4 = off[k] + 8 * t + 4 * h + r;
-                    for (int ct = 0; ct < CT; ++ct) {
-                        const int c = 8 * ct + g;
-                        double v = 0.0;
-                        if (i4 < off[k + 1]) {
-                            const double *r4 = rec.data() + (size_t)i4 * RS;
-                            if (c < n) v = r4[c];
-                            else if (c == n) v = r4[n];
-                            else if (c == n + 1) v = 1.0;
-                        }
-                        b4[((size_t)(2 * ntg + h) * CT + ct) * 32 + lane] = v;
+                b2p[((size_t)ntg * KS + kk) * 32 + lane] = vp;
+                b2t[((size_t)ntg * KS + kk) * 32 + lane] = vt;
+            }
+            for (int h = 0; h < 2; ++h) { // stage 4: B[r][g] = slot 8t+4h+r, column 8ct+g
+                const int64_t i4 = slot[8 * ntg + 4 * h + r];
+                for (int ct = 0; ct < CT; ++ct) {
+                    const int c = 8 * ct + g;
+                    double v = 0.0;
+                    if (i4 >= 0) {
+                        const double *r4 = rec.data() + (size_t)i4 * RS;
+                        if (c < n) v = r4[c];
+                        else if (c == n) v = r4[n];
+                        else if (c == n + 1) v = 1.0;
                     }
+                    b4[((size_t)(2 * ntg + h) * CT + ct) * 32 + lane] = v;
                 }
             }
         }
@@ -271,13 +316,14 @@ static int build_dense(pht_system *s)
     if ((e = cudaMalloc(&s->d_b2phi, b2p.size() * 8)) != cudaSuccess ||
         (e = cudaMalloc(&s->d_b2th, b2t.size() * 8)) != cudaSuccess ||
         (e = cudaMalloc(&s->d_b4, b4.size() * 8)) != cudaSuccess ||
-        (e = cudaMalloc(&s->d_ntoff, ntoff.size() * sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&s->d_tinfo, tinfo.size() * sizeof(int))) != cudaSuccess ||
         (e = cudaMemcpy(s->d_b2phi, b2p.data(), b2p.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(s->d_b2th, b2t.data(), b2t.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
         (e = cudaMemcpy(s->d_b4, b4.data(), b4.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaMemcpy(s->d_ntoff, ntoff.data(), ntoff.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess)
+        (e = cudaMemcpy(s->d_tinfo, tinfo.data(), tinfo.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess)
         return e == cudaErrorMemoryAllocation ? PHT_ENOMEM : cuda_fail(e);
     s->max_ntk = max_ntk;
+    s->dense_ntiles = NT;
     s->dense = 1;
     return PHT_OK;
 }
@@ -397,7 +443,7 @@ extern "C" void pht_system_destroy(pht_system *s)
     cudaFree(s->d_b2phi);
     cudaFree(s->d_b2th);
     cudaFree(s->d_b4);
-    cudaFree(s->d_ntoff);
+    cudaFree(s->d_tinfo);
     cudaFree(s->ws);
     for (int u = 0; u < 3; ++u) {
         if (s->hs[u]) cudaStreamDestroy(s->hs[u]);
@@ -611,7 +657,7 @@ static int dispatch(const pht_system *s, int mode, const pht::Args &A0, void *st
         else if (fam == PHT_KERNELS_AUTO || fam == PHT_KERNELS_SPECIALIZED) dense = s->n > 12;
     }
     const int lfam = fam == PHT_KERNELS_TILE ? pht::FAM_TILE : pht::FAM_AUTO;
-    const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_ntoff, s->max_ntk};
+    const pht::DenseSys D{s->d_b2phi, s->d_b2th, s->d_b4, s->d_tinfo, s->dense_ntiles, s->max_ntk};
     // point-per-lane evaluation (k_evalw): LANE for n <= 12, AUTO for 6 <= n <= 12 (measured, one B200,
     // G points/s: cyclic-10 1.06 vs 0.76 warp-per-group vs 0.62 tensor cores, noon-10 0.96 / 0.71 /
     // 0.61, katsura-10 (n = 11) 0.70 / 0.44 / 0.58; cyclic-5 2.85 vs 3.31 for the warp-per-group

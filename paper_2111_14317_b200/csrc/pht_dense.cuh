@@ -6,7 +6,8 @@
 // Laurent n=20, 50 terms per equation).  sm_100a has no f64 tcgen05 kind; FP64 tensor work is
 // mma.sync.m8n8k4.f64 (SASS DMMA), measured at 37.1 TFLOP/s on B200 (profiles/r01_microbench).
 //
-// Per warp: NMT M-tiles of 8 points.  Per equation k, its terms are streamed in n-tiles of 8:
+// Per warp: NMT M-tiles of 8 points.  The terms of all equations are streamed in n-tiles of 8
+// slots (a tile may end one equation and start the next: segments A = [0, sb), B = [sb, 8)):
 //   stage 2  Phi(8 pts x 8 terms)   = [rho | tau | 1 | 0]   (8 x KP) . B_phi(KP x 8)   (DMMA)
 //            Theta(8 pts x 8 terms) = [theta | 0 | 1 | 0] (8 x KP) . B_th (KP x 8)    (DMMA)
 //            with B_phi rows = (a_i, omega_i, log|c_i|), B_th rows = (a_i, 0, arg c_i)
@@ -27,15 +28,16 @@
 namespace pht {
 
 struct DenseSys {
-    const double *b2phi;   // [sum_k ntk][KS][32]
-    const double *b2th;    // [sum_k ntk][KS][32]
-    const double *b4;      // [sum_k 2*ntk][CT][32]
-    const int *ntile_off;  // [n+1] prefix sums of ntk (n-tiles of 8 terms per equation)
-    int max_ntk;           // max_k ntk: size of one equation's staged B tiles
+    const double *b2phi;   // [ntiles][KS][32]
+    const double *b2th;    // [ntiles][KS][32]
+    const double *b4;      // [2*ntiles][CT][32]
+    const int *tinfo;      // [2n] per equation: ts | te << 16, sb | done << 8 | endB << 9 (build_dense)
+    int ntiles;            // n-tiles of 8 slots of the packed term stream
+    int chunk;             // most n-tiles one equation processes: size of its staged B operands
 };
 
-// doubles of one equation's B operands staged in shared memory: b2phi, b2th (ntk x KS x 32) and
-// b4 (2 ntk x CT x 32), for ntk = max_ntk
+// doubles of one n-tile's B operands staged in shared memory: b2phi, b2th (KS x 32) and
+// b4 (2 x CT x 32); an equation's staged range holds at most D.chunk tiles
 template <int N>
 __host__ __device__ constexpr int dense_eq_doubles_per_tile()
 {
@@ -177,9 +179,12 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
     // warps of the CTA share them instead of each streaming them from L2 (ncu: long-scoreboard
     // stalls on the B loads were the first limiter)
     double *bbuf = reinterpret_cast<double *>(smem_raw + ((sizeof(DenseSmem<N>) + 15) & ~(size_t)15));
-    const int EQB = D.max_ntk * dense_eq_doubles_per_tile<N>();
+    const int EQB = D.chunk * dense_eq_doubles_per_tile<N>();
+    // equation k processes the n-tiles [ts, te) of the packed stream: the tiles that start with
+    // its terms, plus (when it ends inside a tile where equation k + 1 starts) that boundary tile
+    // (build_dense: einfo[2k] = ts | te << 16, einfo[2k + 1] = sb | done << 8 | endB << 9)
     auto stage = [&](int k, int buf) {
-        const int t0 = __ldg(D.ntile_off + k), nt = __ldg(D.ntile_off + k + 1) - t0;
+        const int rg = __ldg(D.tinfo + 2 * k), t0 = rg & 0xffff, nt = (rg >> 16) - t0;
         double *dst = bbuf + (size_t)buf * EQB;
         const int n2 = nt * KS * 32, n4 = 2 * nt * CT * 32; // doubles per segment (multiples of 32)
         const double *s0 = D.b2phi + (size_t)t0 * KS * 32, *s1 = D.b2th + (size_t)t0 * KS * 32,
@@ -195,9 +200,22 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
         stage(0, 0);
         cp_async_commit();
     }
-
+    // stage-4 accumulators [m][ct][re/im][2] of the current equation (carried into the next one
+    // when it starts inside a boundary tile)
+    double acc[NMT][CT][2][2];
+    double ed[NMT], eh[NMT], el[NMT]; // per-point row exponent of the current equation (row g)
+#pragma unroll
+    for (int m = 0; m < NMT; ++m) {
+        ed[m] = -1e300;
+#pragma unroll
+        for (int ct = 0; ct < CT; ++ct)
+            acc[m][ct][0][0] = acc[m][ct][0][1] = acc[m][ct][1][0] = acc[m][ct][1][1] = 0.0;
+    }
+#pragma unroll 1
     for (int k = 0; k < N; ++k) {
-        const int nt0 = __ldg(D.ntile_off + k), nt1 = __ldg(D.ntile_off + k + 1);
+        const int rg = __ldg(D.tinfo + 2 * k), fl = __ldg(D.tinfo + 2 * k + 1);
+        const int ts = rg & 0xffff, te = rg >> 16, sb = fl & 0xff;
+        const bool done = (fl >> 8) & 1, endB = (fl >> 9) & 1;
         if (NB == 2) {
             if (k + 1 < N) stage(k + 1, (k + 1) & 1);
             cp_async_commit();
@@ -208,24 +226,16 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
             cp_async_wait<0>();
         }
         __syncthreads(); // ... and everyone else's
+        if (!done) {
         const double *bk = bbuf + (size_t)(NB == 2 ? (k & 1) : 0) * EQB;
-        const int n2k = (nt1 - nt0) * KS * 32;
-        // stage-4 accumulators [m][ct][re/im][2]
-        double acc[NMT][CT][2][2];
-        double ed[NMT], eh[NMT], el[NMT]; // per-point row exponent (this thread's row g)
-#pragma unroll
-        for (int m = 0; m < NMT; ++m) {
-            ed[m] = -1e300;
-#pragma unroll
-            for (int ct = 0; ct < CT; ++ct)
-                acc[m][ct][0][0] = acc[m][ct][0][1] = acc[m][ct][1][0] = acc[m][ct][1][1] = 0.0;
-        }
-        for (int nt = nt0; nt < nt1; ++nt) {
-            // stage 2: phi and theta tiles for the 8 terms of this n-tile
-            double ph[NMT][2], th[NMT][2];
+        const int n2k = (te - ts) * KS * 32;
+        const bool bnd = sb < 8;           // the last tile is a boundary tile
+        const int tf = bnd ? te - 1 : te;  // tiles [ts, tf) hold equation k only
+        // stage 2 of tile nt: phi and theta for its 8 slots
+        auto stage2 = [&](int nt, double (&ph)[NMT][2], double (&th)[NMT][2]) {
 #pragma unroll
             for (int m = 0; m < NMT; ++m) ph[m][0] = ph[m][1] = th[m][0] = th[m][1] = 0.0;
-            const double *bp = bk + ((size_t)(nt - nt0) * KS) * 32 + lane;
+            const double *bp = bk + ((size_t)(nt - ts) * KS) * 32 + lane;
             const double *bt = bp + n2k;
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk) {
@@ -236,38 +246,69 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
                     dmma(th[m][0], th[m][1], aT[m][kk], vt);
                 }
             }
-            // stage 3: online row exponent per point (row g is shared by the quad) and exp*cis
+        };
+        // online row exponent of the current equation from a quad maximum key (row g is shared
+        // by the quad): the first tile sets it, a term more than e^512 above rescales exactly
+        auto row_exp = [&](int m, int kx) {
+            kx = max(kx, __shfl_xor_sync(0xffffffffu, kx, 1));
+            kx = max(kx, __shfl_xor_sync(0xffffffffu, kx, 2));
+            const double mx = dkey_hi_inv(kx);
+            if (ed[m] == -1e300) {
+                ed[m] = isfinite(mx) ? rint(mx * KC[14]) : 0.0;
+                eh[m] = ed[m] * KC[12];
+                el[m] = ed[m] * KC[13];
+            } else if ((mx - eh[m]) - el[m] > 512.0) {
+                const double e2 = rint(mx * KC[14]);
+                // two normal factors (see RowAcc::reduce): one 2^d underflows for d < -1074
+                const int d = (int)fmax(ed[m] - e2, -2000.0), d1 = d / 2;
+                const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d - d1);
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        acc[m][ct][u][0] = acc[m][ct][u][0] * f1 * f2;
+                        acc[m][ct][u][1] = acc[m][ct][u][1] * f1 * f2;
+                    }
+                ed[m] = e2;
+                eh[m] = e2 * KC[12];
+                el[m] = e2 * KC[13];
+            }
+        };
+        // stage 4, k-step h of tile nt: A operand W[row g][slot 4h + r] from the quad, zero
+        // outside the slot range [lo, hi)
+        auto stage4 = [&](int nt, int h, const double (&wr)[NMT][2], const double (&wi)[NMT][2], int lo, int hi,
+                          bool masked) {
+            const int jt = 4 * h + r;                // slot of this lane's A element
+            const int src = (lane & ~3) | (jt >> 1); // quad lane holding it
+            const bool keep = !masked || (jt >= lo && jt < hi);
+            const double *b4 = bk + 2 * n2k + ((size_t)(2 * (nt - ts) + h) * CT) * 32 + lane;
+            double bv[CT];
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct) bv[ct] = b4[ct * 32];
+#pragma unroll
+            for (int m = 0; m < NMT; ++m) {
+                const double r0 = __shfl_sync(0xffffffffu, wr[m][0], src);
+                const double r1 = __shfl_sync(0xffffffffu, wr[m][1], src);
+                const double i0 = __shfl_sync(0xffffffffu, wi[m][0], src);
+                const double i1 = __shfl_sync(0xffffffffu, wi[m][1], src);
+                const double ar = keep ? ((jt & 1) ? r1 : r0) : 0.0, ai = keep ? ((jt & 1) ? i1 : i0) : 0.0;
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct) {
+                    dmma(acc[m][ct][0][0], acc[m][ct][0][1], ar, bv[ct]);
+                    dmma(acc[m][ct][1][0], acc[m][ct][1][1], ai, bv[ct]);
+                }
+            }
+        };
+        for (int nt = ts; nt < tf; ++nt) { // tiles of equation k only (the common case)
+            double ph[NMT][2], th[NMT][2];
+            stage2(nt, ph, th);
+            // stage 3: row exponent (row maximum on the integer pipe: the high words of the
+            // doubles as a monotone integer key; measured: the FP64 DSETP.MAX chain was the
+            // hottest stall of the kernel, on the datapath DMMA shares) and exp*cis
             double wr[NMT][2], wi[NMT][2];
 #pragma unroll
             for (int m = 0; m < NMT; ++m) {
-                // row maximum on the integer pipe: the high words of the doubles in a monotone
-                // integer key (sign-magnitude -> two's complement); the row exponent only needs the
-                // maximum to ~2^-20 relative (measured: the FP64 DSETP.MAX chain was the hottest
-                // stall of the kernel, on the datapath DMMA shares)
-                int kx = max(dkey_hi(ph[m][0]), dkey_hi(ph[m][1]));
-                kx = max(kx, __shfl_xor_sync(0xffffffffu, kx, 1));
-                kx = max(kx, __shfl_xor_sync(0xffffffffu, kx, 2));
-                const double mx = dkey_hi_inv(kx);
-                if (ed[m] == -1e300) { // first n-tile: set the exponent from the leading term
-                    ed[m] = isfinite(mx) ? rint(mx * KC[14]) : 0.0;
-                    eh[m] = ed[m] * KC[12];
-                    el[m] = ed[m] * KC[13];
-                } else if ((mx - eh[m]) - el[m] > 512.0) { // exact power-of-two rescale
-                    const double e2 = rint(mx * KC[14]);
-                    // two normal factors (see RowAcc::reduce): one 2^d underflows for d < -1074
-                    const int d = (int)fmax(ed[m] - e2, -2000.0), d1 = d / 2;
-                    const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d - d1);
-#pragma unroll
-                    for (int ct = 0; ct < CT; ++ct)
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            acc[m][ct][u][0] = acc[m][ct][u][0] * f1 * f2;
-                            acc[m][ct][u][1] = acc[m][ct][u][1] * f1 * f2;
-                        }
-                    ed[m] = e2;
-                    eh[m] = e2 * KC[12];
-                    el[m] = e2 * KC[13];
-                }
+                row_exp(m, max(dkey_hi(ph[m][0]), dkey_hi(ph[m][1])));
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     const double2 w = expcis((ph[m][u] - eh[m]) - el[m], th[m][u], sm.exptab, sm.cistab);
@@ -275,61 +316,85 @@ __global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S
                     wi[m][u] = w.y;
                 }
             }
-            // stage 4: two k-steps of 4 terms; A operand W[row g][term 4h + r] from the quad
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int jt = 4 * h + r;              // term of this lane's A element
-                const int src = (lane & ~3) | (jt >> 1); // quad lane holding it
-                const double *b4 = bk + 2 * n2k + ((size_t)(2 * (nt - nt0) + h) * CT) * 32 + lane;
-                double bv[CT];
+            for (int h = 0; h < 2; ++h) stage4(nt, h, wr, wi, 0, 8, false);
+        }
+        // the boundary tile: slots [0, sb) end equation k, [sb, 8) start equation k + 1 (its own
+        // exponent from its own maximum); W of the boundary tile kept across equation k's epilogue
+        double wr[NMT][2], wi[NMT][2], edB[NMT];
+        if (bnd) {
+            double ph[NMT][2], th[NMT][2];
+            stage2(te - 1, ph, th);
+            const bool inA0 = 2 * r < sb, inA1 = 2 * r + 1 < sb;
+            constexpr int KMIN = (int)0x80000000;
 #pragma unroll
-                for (int ct = 0; ct < CT; ++ct) bv[ct] = b4[ct * 32];
+            for (int m = 0; m < NMT; ++m) {
+                const int k0 = dkey_hi(ph[m][0]), k1 = dkey_hi(ph[m][1]);
+                row_exp(m, max(inA0 ? k0 : KMIN, inA1 ? k1 : KMIN));
+                int kb = max(inA0 ? KMIN : k0, inA1 ? KMIN : k1);
+                kb = max(kb, __shfl_xor_sync(0xffffffffu, kb, 1));
+                kb = max(kb, __shfl_xor_sync(0xffffffffu, kb, 2));
+                const double mb = dkey_hi_inv(kb);
+                edB[m] = isfinite(mb) ? rint(mb * KC[14]) : 0.0;
+                const double bh = edB[m] * KC[12], bl = edB[m] * KC[13];
 #pragma unroll
-                for (int m = 0; m < NMT; ++m) {
-                    const double r0 = __shfl_sync(0xffffffffu, wr[m][0], src);
-                    const double r1 = __shfl_sync(0xffffffffu, wr[m][1], src);
-                    const double i0 = __shfl_sync(0xffffffffu, wi[m][0], src);
-                    const double i1 = __shfl_sync(0xffffffffu, wi[m][1], src);
-                    const double ar = (jt & 1) ? r1 : r0, ai = (jt & 1) ? i1 : i0;
-#pragma unroll
-                    for (int ct = 0; ct < CT; ++ct) {
-                        dmma(acc[m][ct][0][0], acc[m][ct][0][1], ar, bv[ct]);
-                        dmma(acc[m][ct][1][0], acc[m][ct][1][1], ai, bv[ct]);
-                    }
+                for (int u = 0; u < 2; ++u) {
+                    const bool ia = u ? inA1 : inA0;
+                    const double2 w = expcis((ph[m][u] - (ia ? eh[m] : bh)) - (ia ? el[m] : bl), th[m][u],
+                                             sm.exptab, sm.cistab);
+                    wr[m][u] = w.x;
+                    wi[m][u] = w.y;
                 }
             }
         }
-        // epilogue for equation k: this thread holds columns 8ct + 2r + {0,1} of point row g
+        // segment 0: the rest of equation k (the boundary tile's A slots), then its row;
+        // segment 1 (boundary tiles): equation k + 1's first slots, and its row if it ends here
+#pragma unroll 1
+        for (int sg = 0; sg < (bnd ? 2 : 1); ++sg) {
+            if (bnd) {
+                const int lo = sg ? sb : 0, hi = sg ? 8 : sb;
+                for (int h = lo >> 2; h < ((hi + 3) >> 2); ++h) stage4(te - 1, h, wr, wi, lo, hi, true);
+            }
+            if (sg == 1 && !endB) break;
+            // epilogue for equation kr: this thread holds columns 8ct + 2r + {0,1} of point row g
+            const int kr = k + sg;
 #pragma unroll
-        for (int m = 0; m < NMT; ++m) {
-            const int q = (warp * NMT + m) * 8 + g;
-            const int64_t gq = base + q;
-            const int e = (int)ed[m];
-            bool fin = true;
+            for (int m = 0; m < NMT; ++m) {
+                const int q = (warp * NMT + m) * 8 + g;
+                const int64_t gq = base + q;
+                const int e = (int)ed[m];
+                bool fin = true;
 #pragma unroll
-            for (int ct = 0; ct < CT; ++ct)
+                for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int c = 8 * ct + 2 * r + u;
-                    if (c >= N + 2) continue;
-                    double2 v = make_double2(acc[m][ct][0][u], acc[m][ct][1][u]);
-                    if (MODE == MODE_EVAL_X) {
-                        if (c < N) v = cmul(v, sm.inv[q][c]);
-                        else if (c == N) v = make_double2(v.x * sm.tinv[q], v.y * sm.tinv[q]);
+                    for (int u = 0; u < 2; ++u) {
+                        const int cc = 8 * ct + 2 * r + u;
+                        if (cc >= N + 2) continue;
+                        double2 v = make_double2(acc[m][ct][0][u], acc[m][ct][1][u]);
+                        acc[m][ct][0][u] = acc[m][ct][1][u] = 0.0;
+                        if (MODE == MODE_EVAL_X) {
+                            if (cc < N) v = cmul(v, sm.inv[q][cc]);
+                            else if (cc == N) v = make_double2(v.x * sm.tinv[q], v.y * sm.tinv[q]);
+                        }
+                        if (!scaled && e != 0) {
+                            if (e >= -1022 && e <= 1023) v = make_double2(v.x * pow2i(e), v.y * pow2i(e));
+                            else v = make_double2(scalbn(v.x, e), scalbn(v.y, e));
+                        }
+                        fin = fin && isfinite(v.x) && isfinite(v.y);
+                        if (gq < A.P) {
+                            if (cc < N) { if (A.J) A.J[(gq * N + kr) * N + cc] = v; }
+                            else if (cc == N) { if (A.Jt) A.Jt[gq * N + kr] = v; }
+                            else if (A.H) A.H[gq * N + kr] = v;
+                        }
                     }
-                    if (!scaled && e != 0) {
-                        if (e >= -1022 && e <= 1023) v = make_double2(v.x * pow2i(e), v.y * pow2i(e));
-                        else v = make_double2(scalbn(v.x, e), scalbn(v.y, e));
-                    }
-                    fin = fin && isfinite(v.x) && isfinite(v.y);
-                    if (gq < A.P) {
-                        if (c < N) { if (A.J) A.J[(gq * N + k) * N + c] = v; }
-                        else if (c == N) { if (A.Jt) A.Jt[gq * N + k] = v; }
-                        else if (A.H) A.H[gq * N + k] = v;
-                    }
-                }
-            if (!fin) atomicOr(&sm.st[q], PT_NONFINITE);
-            if (scaled && r == 0 && gq < A.P) A.rexp[gq * N + k] = e;
+                if (!fin) atomicOr(&sm.st[q], PT_NONFINITE);
+                if (scaled && r == 0 && gq < A.P) A.rexp[gq * N + kr] = e;
+                // the next equation: the boundary tile's B exponent, else fresh
+                ed[m] = (sg == 0 && bnd) ? edB[m] : -1e300;
+                eh[m] = ed[m] * KC[12];
+                el[m] = ed[m] * KC[13];
+            }
+        }
         }
         __syncthreads(); // buffer (k & 1) is refilled by the prefetch of equation k + 2
     }
@@ -345,7 +410,7 @@ cudaError_t launch_dense_mode(const DevSys &S, const DenseSys &D, const Args &A,
     const int64_t tiles = (A.P + PTS - 1) / PTS;
     if (tiles == 0) return cudaSuccess;
     const size_t sb = ((sizeof(DenseSmem<N>) + 15) & ~(size_t)15) +
-                      (size_t)DGeo<N>::NBUF * D.max_ntk * dense_eq_doubles_per_tile<N>() * sizeof(double);
+                      (size_t)DGeo<N>::NBUF * D.chunk * dense_eq_doubles_per_tile<N>() * sizeof(double);
     // the staged B tiles make the size system dependent: set the attribute to the largest seen
     static std::atomic<size_t> configured_sb[64];
     int dev = 0;

@@ -514,6 +514,12 @@ struct PointLog<N, false> {
     }
     __device__ __forceinline__ double2 get(int j) const { return make_double2(rho[j], th[j]); }
 };
+// PHT_RT_VOL (experiments): 1 = every term re-reads (rho, vartheta) from shared memory (volatile
+// loads the compiler cannot hoist out of the term loop: 4N fewer live registers); 2 = only rho
+// re-read, vartheta hoisted
+#ifndef PHT_RT_VOL
+#define PHT_RT_VOL 0
+#endif
 template <int N>
 struct PointLog<N, true> {
     const double2 *base;
@@ -524,7 +530,22 @@ struct PointLog<N, true> {
         base = &rt[0][q];
         stride = WL;
     }
-    __device__ __forceinline__ double2 get(int j) const { return base[j * stride]; }
+    __device__ __forceinline__ double2 get(int j) const
+    {
+#if PHT_RT_VOL == 1
+        double2 v;
+        const unsigned a = (unsigned)__cvta_generic_to_shared(base + j * stride);
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+        return v;
+#elif PHT_RT_VOL == 2
+        double r;
+        const unsigned a = (unsigned)__cvta_generic_to_shared(base + j * stride);
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(a));
+        return make_double2(r, base[j * stride].y);
+#else
+        return base[j * stride];
+#endif
+    }
 };
 
 // phi = omega tau + log|c| + sum_j a_j rho_j and theta = arg c + sum_j a_j vartheta_j, each with

@@ -309,6 +309,40 @@ def test_dense_tensor_core_evaluate(P, n, m, p):
     assert be[st2.cpu().numpy() == 0].max() <= 1e-10
 
 
+@pytest.mark.parametrize("counts", [(1, 3, 9, 2, 14, 8), (8, 8, 5, 3, 11, 1, 2, 16, 7, 6),
+                                    (2, 2, 2, 2, 2, 2, 2), (13, 50, 4, 27, 3, 9, 8, 1)])
+def test_dense_packed_tiles_ragged_equations(P, counts):
+    """The DMMA path streams the terms of all equations in n-tiles of 8 slots: a tile may end one
+    equation and start the next (build_dense; at most one start inside a tile, a second is moved to
+    the next tile behind padding slots).  Ragged term counts exercise every case: equations shorter
+    than a tile, ending exactly at a tile end, a second boundary forcing padding, one-term rows.
+    Against the oracle at <= 1e-10 (term-sum metric), unscaled, scaled and log variants."""
+    n = len(counts)
+    rng = np.random.Generator(np.random.PCG64(sum(counts)))
+    eqs = []
+    for m in counts:
+        seen = set()
+        while len(seen) < m:
+            seen.add(tuple(int(v) for v in rng.integers(-2, 3, size=n)))
+        eqs.append([(a, 1.0) for a in sorted(seen)])
+    sysm = W.from_terms(f"ragged-{n}", n, eqs, seed=n, lift_max=20)
+    g = P.System.from_workload(sysm).set_kernels("dense")
+    x, t, _ = W.random_points(93, n, seed=6, rho_max=0.5)
+    o = oracle.Oracle(sysm).evaluate(x, t)
+    H, Jx, Jt, st = g.evaluate(_cuda(x), _cuda(t))
+    assert np.all(st.cpu().numpy() == 0)
+    assert eval_err(H.cpu().numpy(), o["H"], o["SH"]) <= 1e-10
+    assert eval_err(Jx.cpu().numpy(), o["Jx"], o["SJx"]) <= 1e-10
+    assert eval_err(Jt.cpu().numpy(), o["Jt"], o["SJt"]) <= 1e-10
+    Hs, Jxs, Jts, e2, _ = g.evaluate(_cuda(x), _cuda(t), scaled=True)
+    sc = np.exp2(e2.cpu().numpy().astype(float))
+    assert eval_err(Jxs.cpu().numpy() * sc[:, :, None], o["Jx"], o["SJx"]) <= 1e-10
+    Hl, Jz, Jtau, e2l, _ = g.evaluate_log(_cuda(np.log(x)), _cuda(np.log(t)))
+    scl = np.exp2(e2l.cpu().numpy().astype(float))
+    assert eval_err(Hl.cpu().numpy() * scl, o["H"], o["SH"]) <= 1e-10
+    assert eval_err(Jz.cpu().numpy() * scl[:, :, None], o["Jx"] * x[:, None, :], o["SJx"] * np.abs(x)[:, None, :]) <= 1e-10
+
+
 @pytest.mark.parametrize("family", ["tile", "dense", "specialized", "lane"])
 def test_row_rescale_keeps_entries_far_below_the_row(P, family):
     """Regression (found by the C5 range-stress test): the online row rescale by 2^d with
