@@ -160,6 +160,37 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def host_link_bound(dev, bin_, bout):
+    """ms to move bin_ bytes host->device and bout bytes device->host concurrently (pinned host
+    memory, one stream per direction, no kernel): the floor of the end-to-end step time."""
+    import torch
+    hi = torch.empty(bin_, dtype=torch.uint8).pin_memory()
+    ho = torch.empty(bout, dtype=torch.uint8).pin_memory()
+    di = torch.empty(bin_, dtype=torch.uint8, device=dev)
+    do = torch.empty(bout, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = None
+    for _ in range(3):
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream(dev)
+        e0.record(cur)
+        s1.wait_event(e0)
+        s2.wait_event(e0)
+        with torch.cuda.stream(s1):
+            di.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s2):
+            ho.copy_(do, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+        e1.record(cur)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del hi, ho, di, do
+    return best
+
+
 def step_traffic(points):
     """DRAM bytes per step launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
     ncu --set full capture of the same kernel (profiles/r02_step_traffic.json), scaled from the
@@ -723,6 +754,7 @@ def main():
             dist.all_reduce(te_ms, op=dist.ReduceOp.MAX)
         e2e_runs.append(float(te_ms.item()))
     e2e_value = 2.0 * Pn * world * args.e2e_steps / (float(np.median(e2e_runs)) * 1e-3)
+    link = host_link_bound(dev, Pn * (16 * N_VARS + 16), Pn * (16 * N_VARS + 8 + 1 + 8))
 
     peak_mhz = (clk.summary() or {}).get("sm_max_mhz") or 1965.0
     tracking = tracking_section(world, rank, dev, [t for t in args.tracking.split(",") if t],
@@ -757,7 +789,11 @@ def main():
                          "frac_minimal_count": 2 * fl["minimal_total"] * Pn / (ms_step * 1e-3) / 1e12 / peak},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pn * (16 * N_VARS + 16),
                     "d2h_bytes_per_step": Pn * (16 * N_VARS + 8 + 1 + 8),
-                    "runs_ms": e2e_runs, "steps_per_run": args.e2e_steps},
+                    "runs_ms": e2e_runs, "steps_per_run": args.e2e_steps,
+                    # the host link bounds this number: the step's copy-in and copy-out bytes moved
+                    # concurrently (pinned, two streams, no kernel) take link_ms
+                    "link_ms_per_step": link, "frac_of_link_bound":
+                        (link / (float(np.median(e2e_runs)) / args.e2e_steps)) if link else None},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "tracking": tracking,

@@ -97,7 +97,7 @@ struct pht_system {
     int dense = 0;
     double *d_b2phi = nullptr, *d_b2th = nullptr, *d_b4 = nullptr;
     int *d_tinfo = nullptr; // per n-tile equation / boundary info (build_dense)
-    int max_ntk = 0; // tiles per staged chunk of B operands (most n-tiles of one equation)
+    int max_ntk = 0; // most n-tiles one equation processes (k_dense staging size)
     int dense_ntiles = 0; // n-tiles of the packed term stream
     // packed tables on the host (input of the code generator, pht_system_specialize)
     std::vector<double> h_rec;
@@ -110,9 +110,10 @@ struct pht_system {
     std::vector<pht::JitKernels *> jit_old;
     // workspace and copy/compute streams of the *_host entry points
     std::mutex ws_mu;
-    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t hev0 = nullptr;
+    // (copy-in, two compute, copy-out; per-chunk events: copy-in done, kernel done)
+    cudaStream_t hs[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t hev_in[64] = {}, hev_k[64] = {};
+    cudaEvent_t hev0 = nullptr, hev_end = nullptr;
     int64_t ws_cap = 0;
     void *ws = nullptr;
 };
@@ -445,11 +446,14 @@ extern "C" void pht_system_destroy(pht_system *s)
     cudaFree(s->d_b4);
     cudaFree(s->d_tinfo);
     cudaFree(s->ws);
-    for (int u = 0; u < 3; ++u) {
+    for (int u = 0; u < 4; ++u)
         if (s->hs[u]) cudaStreamDestroy(s->hs[u]);
-        if (s->hev[u]) cudaEventDestroy(s->hev[u]);
+    for (int c = 0; c < 64; ++c) {
+        if (s->hev_in[c]) cudaEventDestroy(s->hev_in[c]);
+        if (s->hev_k[c]) cudaEventDestroy(s->hev_k[c]);
     }
     if (s->hev0) cudaEventDestroy(s->hev0);
+    if (s->hev_end) cudaEventDestroy(s->hev_end);
     pht::jit_free(s->jit);
     for (pht::JitKernels *J : s->jit_old) pht::jit_free(J);
     delete s;
@@ -766,19 +770,28 @@ extern "C" int pht_pc_step(const pht_system *s, int64_t p, double *x, double *ta
 }
 
 // Host-buffer step, pipelined (the batch pipelining of P:807-824 as stream
-// overlap): the points are cut into chunks; chunk c runs H2D -> step kernel -> D2H on internal
-// stream c mod PHT_HOST_STREAMS, so the two copy directions and the kernels of different chunks
-// overlap (copy engines and SMs work concurrently; pinned host memory needed for overlap).
-#define PHT_HOST_STREAMS 3
+// overlap): the points are cut into chunks and run through a three-stage stream pipeline --
+// copy-in stream (H2D of every chunk back to back), compute (the step kernel of chunk c once its
+// copy-in event fired; two streams taken alternately so the tail of one chunk's persistent kernel
+// overlaps the start of the next), copy-out stream (D2H of chunk c once its kernel event fired).
+// Each copy engine direction then streams without waiting on the other (pinned host memory needed
+// for overlap).  Round 2 had chunk c's H2D, kernel and D2H in one of 3 round-robin streams, so a
+// chunk's copy-in queued behind the copy-out of the chunk three places earlier.
+#define PHT_HOST_CHUNKS 32
 static int ensure_streams(pht_system *s)
 {
     if (s->hs[0]) return PHT_OK;
-    for (int u = 0; u < PHT_HOST_STREAMS; ++u) {
+    for (int u = 0; u < 4; ++u) {
         cudaError_t e = cudaStreamCreateWithFlags(&s->hs[u], cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->hev[u], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    for (int c = 0; c < 64; ++c) {
+        cudaError_t e = cudaEventCreateWithFlags(&s->hev_in[c], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->hev_k[c], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e);
     }
     cudaError_t e = cudaEventCreateWithFlags(&s->hev0, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->hev_end, cudaEventDisableTiming);
     return e == cudaSuccess ? PHT_OK : cuda_fail(e);
 }
 
@@ -810,38 +823,39 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
            *ddn = (double *)(w + bx + 2 * bt);
     uint8_t *dst = (uint8_t *)(w + bx + 3 * bt);
     cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t sin = s->hs[0], sout = s->hs[3];
     // the caller's stream orders us after its earlier work; we order it after our copies
     if ((e = cudaEventRecord(s->hev0, st)) != cudaSuccess) return cuda_fail(e);
-    for (int u = 0; u < PHT_HOST_STREAMS; ++u)
+    for (int u = 0; u < 4; ++u)
         if ((e = cudaStreamWaitEvent(s->hs[u], s->hev0, 0)) != cudaSuccess) return cuda_fail(e);
-    // chunks: 1/32 of the batch (measured 8 -> 416, 16 -> 453, 32 -> 471, 64 -> 453 M evals/s end
-    // to end on the bench step), at least 32K points (launch and copy latency stay amortised); the
+    // chunks: 1/32 of the batch, at least 32K points (launch and copy latency stay amortised); the
     // pipeline fill (first copy-in) and drain (last copy-out) are one chunk each
-    const int nch = 32;
-    int64_t chunk = (p + nch - 1) / nch;
+    int64_t chunk = (p + PHT_HOST_CHUNKS - 1) / PHT_HOST_CHUNKS;
     if (chunk < 32768) chunk = 32768;
     int c = 0;
     for (int64_t b = 0; b < p; b += chunk, ++c) {
         const int64_t m = (p - b < chunk) ? p - b : chunk;
-        cudaStream_t cs_ = s->hs[c % PHT_HOST_STREAMS];
         const size_t ox = (size_t)b * n * 2, mx = (size_t)m * n * 16, mt = (size_t)m * 8;
-        if ((e = cudaMemcpyAsync(dx + ox, x + ox, mx, cudaMemcpyHostToDevice, cs_)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(dtu + b, tau + b, mt, cudaMemcpyHostToDevice, cs_)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(ddt + b, dtau + b, mt, cudaMemcpyHostToDevice, cs_)) != cudaSuccess)
+        cudaStream_t sk = s->hs[1 + (c & 1)];
+        if ((e = cudaMemcpyAsync(dx + ox, x + ox, mx, cudaMemcpyHostToDevice, sin)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dtu + b, tau + b, mt, cudaMemcpyHostToDevice, sin)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(ddt + b, dtau + b, mt, cudaMemcpyHostToDevice, sin)) != cudaSuccess ||
+            (e = cudaEventRecord(s->hev_in[c], sin)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(sk, s->hev_in[c], 0)) != cudaSuccess)
             return cuda_fail(e);
-        rc = pht_pc_step(s, m, dx + ox, dtu + b, ddt + b, newton_iters, dst + b, ddn + b, (void *)cs_);
+        rc = pht_pc_step(s, m, dx + ox, dtu + b, ddt + b, newton_iters, dst + b, ddn + b, (void *)sk);
         if (rc != PHT_OK) return rc;
-        if ((e = cudaMemcpyAsync(x + ox, dx + ox, mx, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(tau + b, dtu + b, mt, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess ||
-            (status && (e = cudaMemcpyAsync(status + b, dst + b, (size_t)m, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess) ||
-            (dn_norm && (e = cudaMemcpyAsync(dn_norm + b, ddn + b, mt, cudaMemcpyDeviceToHost, cs_)) != cudaSuccess))
+        if ((e = cudaEventRecord(s->hev_k[c], sk)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(sout, s->hev_k[c], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(x + ox, dx + ox, mx, cudaMemcpyDeviceToHost, sout)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(tau + b, dtu + b, mt, cudaMemcpyDeviceToHost, sout)) != cudaSuccess ||
+            (status && (e = cudaMemcpyAsync(status + b, dst + b, (size_t)m, cudaMemcpyDeviceToHost, sout)) != cudaSuccess) ||
+            (dn_norm && (e = cudaMemcpyAsync(dn_norm + b, ddn + b, mt, cudaMemcpyDeviceToHost, sout)) != cudaSuccess))
             return cuda_fail(e);
     }
-    for (int u = 0; u < PHT_HOST_STREAMS && u < c; ++u) {
-        if ((e = cudaEventRecord(s->hev[u], s->hs[u])) != cudaSuccess ||
-            (e = cudaStreamWaitEvent(st, s->hev[u], 0)) != cudaSuccess)
-            return cuda_fail(e);
-    }
+    // every chunk's copy-out is on sout, after its kernel; the caller's stream waits for the last
+    if ((e = cudaEventRecord(s->hev_end, sout)) != cudaSuccess || (e = cudaStreamWaitEvent(st, s->hev_end, 0)) != cudaSuccess)
+        return cuda_fail(e);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
     return PHT_OK;
 }
