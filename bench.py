@@ -505,8 +505,9 @@ def tracking_section(world, rank, dev, which, peak_tflops, cpu=True):
             torch.cuda.synchronize(dev)
             ms = torch.tensor([e0.elapsed_time(e2), e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
             if world > 1:   # per-rank times (outside the timed region)
-                allms = torch.empty((world, 2), dtype=torch.float64, device=dev)
+                allms = torch.empty(world * 2, dtype=torch.float64, device=dev)   # flat: nccl and gloo
                 dist.all_gather_into_tensor(allms, ms)
+                allms = allms.reshape(world, 2)
             else:
                 allms = ms[None]
             allms = allms.cpu().numpy()
@@ -664,6 +665,11 @@ def main():
     ap.add_argument("--specialize", action="store_true", help="system-specialised kernels (pht_system_specialize)")
     ap.add_argument("--tracking", default="katsura-10,noon-10,cyclic-10",
                     help="comma list of tracked configs ('' to skip)")
+    # test mode only (tests/test_gpu_bench_ranks.py): run the N-rank flow -- sharding, per-rank
+    # timing, the one gather, rank 0's line -- on a box with fewer GPUs.  The ranks' kernels are
+    # independent (no rank waits on another inside a kernel); gloo carries the collectives.
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help=argparse.SUPPRESS)
+    ap.add_argument("--all-on-device0", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         sys.exit(launch_ranks(args.gpus))
@@ -677,7 +683,9 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
+    if args.all_on_device0:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2111_14317_b200 as P
