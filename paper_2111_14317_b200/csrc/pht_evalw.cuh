@@ -64,7 +64,7 @@ struct SmemEW {
         alignas(16) double sh[32][2];
         double2 inv[N][33]; // 1/x_j of the warp's points (EVAL_X), padded against bank conflicts
     } w[GeoEW<N>::WARPS];
-    // followed by the records R[MT][N][RecW<N>::U] (16-byte units), 16-byte aligned
+    // followed by the records R[MT][N][RecW<N, WIDE>::U] (16-byte units, the packer's doubles), 16-byte aligned
 };
 
 __device__ __forceinline__ void tma_store3(const CUtensorMap *map, const void *smem, int c0, int c1, int c2)
@@ -76,7 +76,8 @@ __device__ __forceinline__ void tma_store3(const CUtensorMap *map, const void *s
                  : "memory");
 }
 
-template <int N, int MODE>
+// WIDE: term records as the packer's doubles (RecW); compact int16 records when those do not fit
+template <int N, int MODE, bool WIDE = true>
 __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
     k_evalw(const DevSys S, const Args A, int MT, const __grid_constant__ EvalMaps M)
 {
@@ -91,12 +92,12 @@ __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
     for (int idx = tid; idx < MT * N; idx += GeoEW<N>::NT) { // records, equation-major per term slot
         const int kk = idx % N, t = idx / N;
         const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
-        if (t < m) pack_rec_w<N>(S.rec + (size_t)(i0 + t) * (RS / 2), R + (size_t)idx * RecW<N>::U);
+        if (t < m) pack_rec_w<N, WIDE>(S.rec + (size_t)(i0 + t) * (RS / 2), R + (size_t)idx * RecW<N, WIDE>::U);
     }
     if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
     __syncthreads();
     typename SmemEW<N>::Warp &W = sm.w[wi];
-    constexpr size_t TS = (size_t)N * RecW<N>::U; // record stride between terms of one equation
+    constexpr size_t TS = (size_t)N * RecW<N, WIDE>::U; // record stride between terms of one equation
     const int64_t groups = (A.P + 31) / 32;
     bool pending = false; // a TMA store of this warp's staging may still read it
     for (int64_t grp = (int64_t)blockIdx.x * GeoEW<N>::WARPS + wi; grp < groups;
@@ -140,18 +141,18 @@ __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
         for (int k = 0; k < N; ++k) {
             // a2-a4 for row k of this lane's point: every lane reads the same records (broadcast)
             const int m = sm.mk[k];
-            const double2 *rec = R + (size_t)k * RecW<N>::U;
+            const double2 *rec = R + (size_t)k * RecW<N, WIDE>::U;
             RowAcc<N> acc;
             {
                 double a[RS];
-                load_rec_s<N>(rec, a);
+                load_rec_s<N, WIDE>(rec, a);
                 acc.init(phi_of<N>(a, pl, tau));
             }
             int i = 0;
             for (; PHT_EVALW_PAIR && i + 1 < m; i += 2) { // two terms per iteration (ILP)
                 double a[RS], b[RS];
-                load_rec_s<N>(rec + (size_t)i * TS, a);
-                load_rec_s<N>(rec + (size_t)(i + 1) * TS, b);
+                load_rec_s<N, WIDE>(rec + (size_t)i * TS, a);
+                load_rec_s<N, WIDE>(rec + (size_t)(i + 1) * TS, b);
                 double pa, ta, pb, tb;
                 phi_theta<N>(a, pl, tau, pa, ta);
                 phi_theta<N>(b, pl, tau, pb, tb);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(GeoEW<N>::NT, GeoEW<N>::MINB)
             }
             for (; i < m; ++i) {
                 double a[RS];
-                load_rec_s<N>(rec + (size_t)i * TS, a);
+                load_rec_s<N, WIDE>(rec + (size_t)i * TS, a);
                 double pa, ta;
                 phi_theta<N>(a, pl, tau, pa, ta);
                 const double ya = acc.reduce(pa);
@@ -231,30 +232,39 @@ bool evalw_eligible(const DevSys &S)
 // driver entry point is unavailable or a pointer is not 16-byte aligned (direct stores then)
 int encode_eval_maps(EvalMaps &M, int n, int64_t P, void *J, void *Jt, void *H);
 
-template <int N, int MODE>
-cudaError_t launch_evalw(const DevSys &S, const Args &A, const EvalMaps &M, cudaStream_t stream)
+template <int N, int MODE, bool WIDE>
+cudaError_t launch_evalw_r(const DevSys &S, const Args &A, const EvalMaps &M, size_t sb, cudaStream_t stream)
 {
     const int64_t groups = (A.P + 31) / 32;
-    if (groups == 0) return cudaSuccess;
-    const size_t sb = ((sizeof(SmemEW<N>) + 15) & ~(size_t)15) + (size_t)S.mt * N * RecW<N>::U * 16;
-    if (sb > 200 * 1024) return cudaErrorNotSupported;
     static std::atomic<int64_t> conf_sb[64], last_sb[64], last_fg[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if ((int64_t)sb > conf_sb[dev & 63].load()) {
-        cudaError_t e = cudaFuncSetAttribute(k_evalw<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        cudaError_t e = cudaFuncSetAttribute(k_evalw<N, MODE, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
         if (e != cudaSuccess) return e;
         conf_sb[dev & 63].store((int64_t)sb);
     }
     int64_t fg = (last_sb[dev & 63].load() == (int64_t)sb) ? last_fg[dev & 63].load() : 0;
     if (fg == 0) {
-        fg = persistent_grid(reinterpret_cast<const void *>(k_evalw<N, MODE>), GeoEW<N>::NT, sb);
+        fg = persistent_grid(reinterpret_cast<const void *>(k_evalw<N, MODE, WIDE>), GeoEW<N>::NT, sb);
         last_fg[dev & 63].store(fg);
         last_sb[dev & 63].store((int64_t)sb);
     }
     const int64_t need = (groups + GeoEW<N>::WARPS - 1) / GeoEW<N>::WARPS;
-    k_evalw<N, MODE><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoEW<N>::NT), sb, stream>>>(S, A, S.mt, M);
+    k_evalw<N, MODE, WIDE><<<dim3((unsigned)(need < fg ? need : fg)), dim3(GeoEW<N>::NT), sb, stream>>>(S, A, S.mt, M);
     return cudaGetLastError();
+}
+
+template <int N, int MODE>
+cudaError_t launch_evalw(const DevSys &S, const Args &A, const EvalMaps &M, cudaStream_t stream)
+{
+    const int64_t groups = (A.P + 31) / 32;
+    if (groups == 0) return cudaSuccess;
+    const size_t base = (sizeof(SmemEW<N>) + 15) & ~(size_t)15;
+    const size_t sw = base + (size_t)S.mt * N * RecW<N, true>::U * 16, sc = base + (size_t)S.mt * N * RecW<N>::U * 16;
+    if (sw <= 200 * 1024) return launch_evalw_r<N, MODE, true>(S, A, M, sw, stream);
+    if (sc <= 200 * 1024) return launch_evalw_r<N, MODE, false>(S, A, M, sc, stream);
+    return cudaErrorNotSupported;
 }
 #endif // !__CUDACC_RTC__
 

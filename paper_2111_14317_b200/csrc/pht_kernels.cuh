@@ -1422,17 +1422,22 @@ struct SmemW {
 #ifndef PHT_W_REC16
 #define PHT_W_REC16 1
 #endif
-template <int N>
+template <int N, bool WIDE = false>
 struct RecW {
-    static constexpr bool C16 = PHT_W_REC16 && N <= 12;     // compact layout (the kernels run for n <= 12)
+    // compact layout (the kernels run for n <= 12); WIDE: the packer's doubles.  The point-per-lane
+    // evaluation k_evalw reads every record as a warp broadcast (one address per LDS.128, 2 cycles),
+    // so the 7 wide loads cost less than 3 compact loads + N int16 -> double conversions on the FP64
+    // pipe per lane (measured cyclic-10 1.11 -> 1.18, noon-10 1.02 -> 1.09 G points/s); the lane-per-
+    // row kernels read N different records per load, where the compact records win
+    static constexpr bool C16 = !WIDE && PHT_W_REC16 && N <= 12;
     static constexpr int U = C16 ? 3 : rec_stride(N) / 2;  // 16-byte units per term
 };
 
 // one record, packer layout (rec_stride(N) doubles from global memory) -> shared-memory layout
-template <int N>
+template <int N, bool WIDE = false>
 __device__ __forceinline__ void pack_rec_w(const double2 *src, double2 *dst)
 {
-    if (RecW<N>::C16) {
+    if (RecW<N, WIDE>::C16) {
         unsigned e[6] = {0u, 0u, 0u, 0u, 0u, 0u};
         for (int j = 0; j < N && j < 12; ++j) {
             const double2 v = __ldg(src + j / 2);
@@ -1464,10 +1469,10 @@ __device__ __forceinline__ void unpack_rec16(const uint4 &u0, const uint4 &u1, c
     a[N + 2] = __hiloint2double((int)u2.w, (int)u2.z);
 }
 
-template <int N>
+template <int N, bool WIDE = false>
 __device__ __forceinline__ void load_rec_s(const double2 *r, double (&a)[rec_stride(N)])
 {
-    if (RecW<N>::C16) {
+    if (RecW<N, WIDE>::C16) {
         const uint4 *u = reinterpret_cast<const uint4 *>(r);
         unpack_rec16<N>(u[0], u[1], u[2], a);
     } else {

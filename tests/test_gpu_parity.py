@@ -411,3 +411,19 @@ def test_misaligned_complex_pointers_are_refused(P):
     H, J, Jt, st2 = g.evaluate(xd, td)
     torch.cuda.synchronize()
     assert bool((st2 == 0).all())
+
+
+@pytest.mark.parametrize("n,m", [(6, 500), (12, 150), (8, 40)])
+def test_lane_evaluation_record_layouts(P, n, m):
+    """k_evalw keeps the term records as doubles in shared memory (warp-broadcast loads) and falls
+    back to the compact int16 records when those would not fit (n = 6 with 500 terms, n = 12 with
+    150 terms per equation); both against the oracle (R9 metric <= 1e-10)."""
+    sysm = W.random_dense(n, m, emax=2 if n < 12 else 1, seed=n + m, lift_max=20)
+    g = P.System.from_workload(sysm).set_kernels("lane")
+    x, t, _ = W.random_points(67, n, seed=2, rho_max=0.3)
+    o = oracle.Oracle(sysm).evaluate(x, t)
+    H, Jx, Jt, st = g.evaluate(_cuda(x), _cuda(t))
+    assert np.all(st.cpu().numpy() == 0)
+    assert eval_err(H.cpu().numpy(), o["H"], o["SH"]) <= 1e-10
+    assert eval_err(Jx.cpu().numpy(), o["Jx"], o["SJx"]) <= 1e-10
+    assert eval_err(Jt.cpu().numpy(), o["Jt"], o["SJt"]) <= 1e-10
