@@ -2093,7 +2093,8 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
         stage1<N, LOGS ? MODE_EVAL_Z : MODE_STEP>(sm, tid);
         if (tid < WL && tid >= PTS)
             for (int j = 0; j < N; ++j) sm.rt[j][tid] = make_double2(0.0, 0.0);
-        // any slot in the final refinement: the compensated stage 2 for the whole tile (R30)
+        // any slot in the final refinement: the compensated stage 2 (R30) for the rows of those
+        // slots only (per point: a path's arithmetic never depends on the other slots' phases)
         const int comp = __syncthreads_or(tid < PTS && T.phase[tid] == PH_FINAL);
         if (k < N) {
             double2 row[N + 2];
@@ -2103,7 +2104,7 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
             eval_row<N>(S, sm, k, q, row, e, wq); // generated rows: no compensated variant (FLOOR possible)
             (void)comp;
 #else
-            if (comp) eval_row<N, true>(S, sm, k, q, row, e, wq);
+            if (comp && q < PTS && T.phase[q] == PH_FINAL) eval_row<N, true>(S, sm, k, q, row, e, wq);
             else eval_row<N>(S, sm, k, q, row, e, wq);
 #endif
             if (q < PTS) store_row<N>(sm, k, q, row);
@@ -2256,7 +2257,8 @@ struct SmemTW {
 // COMP: compensated stage 2 (phi_theta_c) for the final refinement at t = 1 (reading R30).
 template <int N, int LPR, bool COMP = false>
 __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const double2 *R, const TrackW<N, LPR> &W,
-                                            int k, int q, int h, const double *wq, double2 (&row)[N + 2], int &e)
+                                            int k, int q, int h, const double *wq, double2 (&row)[N + 2], int &e,
+                                            unsigned mask = 0xffffffffu) // lanes executing this call (LPR shuffles)
 {
     constexpr int RS = rec_stride(N), PPW = GeoTW<N, LPR>::PPW;
     PointLog<N, true> pl;
@@ -2326,14 +2328,14 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
     for (int off = 1; off < LPR; off <<= 1) {
         // align to the larger row exponent (two normal power-of-two factors, see RowAcc::reduce),
         // then add the partner's partial row
-        const double eo = __shfl_xor_sync(0xffffffffu, ed, off), em = fmax(ed, eo);
+        const double eo = __shfl_xor_sync(mask, ed, off), em = fmax(ed, eo);
         const int d = (int)fmax(ed - em, -2000.0), d1 = d / 2;
         const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d - d1);
 #pragma unroll
         for (int c = 0; c < N + 2; ++c) {
             const double2 v = make_double2(row[c].x * f1 * f2, row[c].y * f1 * f2);
-            row[c] = make_double2(v.x + __shfl_xor_sync(0xffffffffu, v.x, off),
-                                  v.y + __shfl_xor_sync(0xffffffffu, v.y, off));
+            row[c] = make_double2(v.x + __shfl_xor_sync(mask, v.x, off),
+                                  v.y + __shfl_xor_sync(mask, v.y, off));
         }
         ed = em;
     }
@@ -2423,12 +2425,23 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             double2 a[N + 2];
             int e;
             const double *wq = A.cellw ? A.cellw + (size_t)W.cell[q] * A.M : nullptr;
-            // the final refinement at t = 1 evaluates with the compensated stage 2 (reading R30):
-            // warp-uniform choice, a few % of the iterations
-            if (__any_sync(0xffffffffu, lane < PPW && W.phase[lane] == PH_FINAL))
-                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e);
-            else
+            // the final refinement at t = 1 evaluates with the compensated stage 2 (reading R30),
+            // chosen per slot: a slot's arithmetic never depends on the phases of the other slots
+            // of its warp (a warp-uniform choice made the endpoints of paths that shared a warp with
+            // a finishing path differ in the last bits from run to run).  A mixed warp runs the two
+            // variants one after the other (a few % of the iterations); the LPR lanes of a row
+            // belong to one slot, so their shuffles stay inside one branch.
+            const bool fin = W.phase[q] == PH_FINAL;
+            const unsigned bal = __ballot_sync(0xffffffffu, fin);
+            if (bal == 0u)
                 eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e);
+            else if (bal == 0xffffffffu)
+                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e);
+            else if (fin)
+                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e, bal);
+            else
+                eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e, ~bal);
+            __syncwarp();
             normalize_row<N>(a);
             int col;
             double2 dE, dN;

@@ -72,6 +72,31 @@ def test_track_deterministic_and_order_invariant(P):
     assert np.array_equal(xa[perm], xb) and np.array_equal(sa[perm], sb)
 
 
+@pytest.mark.parametrize("name,L", [("noon-10", 10_000), ("cyclic-10", 1_000_000)])
+def test_track_cells_bitwise_deterministic(P, name, L):
+    """Every start path tracked twice, the second time in a permuted order (so it shares its warp
+    with other paths): statuses, endpoints and statistics identical bit for bit.  A path's
+    arithmetic depends on its own data only -- regression: the compensated final-refinement
+    evaluation was once chosen per warp, so a path sharing a warp with a finishing path took it
+    too and ~60-85% of the endpoints changed in the last bits from run to run."""
+    from workloads.make_starts import CONFIGS
+    s = CONFIGS[name](L)
+    cells = SS.load_cells(name, L)
+    w0, tau0, cid = SS.start_points_cells(s, cells)
+    wc = _cuda(SS.cell_lifts_fast(s, cells))
+    g = P.System.from_workload(s)
+    perm = np.random.default_rng(3).permutation(len(w0))
+    runs = []
+    for order in (np.arange(len(w0)), perm):
+        z, t = _cuda(w0[order]), _cuda(tau0[order])
+        st, stats = g.track_cells(z, t, wc, _cuda(cid[order]))
+        inv = np.argsort(order)
+        runs.append((z.cpu().numpy()[inv], st.cpu().numpy()[inv], stats.cpu().numpy()[inv]))
+    (za, sa, ka), (zb, sb, kb) = runs
+    assert np.array_equal(sa, sb) and np.array_equal(ka, kb)
+    assert np.array_equal(za.view(np.uint64), zb.view(np.uint64))
+
+
 def test_track_status_isolation(P):
     """batch of 8 with one poisoned start -> 7 converge."""
     sysm = W.from_terms("lin", 1, [[((1,), 1.0, 0), ((0,), -1.0, 1)]], coeffs="native")
