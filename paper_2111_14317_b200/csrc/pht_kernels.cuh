@@ -2255,15 +2255,23 @@ struct SmemTW {
 // the row takes the terms h, h + LPR, ...; the partial rows (each with its own binary row
 // exponent) are aligned to the larger exponent and summed across the LPR lanes (shfl_xor).
 // COMP: compensated stage 2 (phi_theta_c) for the final refinement at t = 1 (reading R30).
+#ifndef PHT_TRACKW_RTREG
+#define PHT_TRACKW_RTREG 0 // experiments: (rho, vartheta) held in registers through the row loop
+#endif
 template <int N, int LPR, bool COMP = false>
 __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const double2 *R, const TrackW<N, LPR> &W,
                                             int k, int q, int h, const double *wq, double2 (&row)[N + 2], int &e,
                                             unsigned mask = 0xffffffffu) // lanes executing this call (LPR shuffles)
 {
     constexpr int RS = rec_stride(N), PPW = GeoTW<N, LPR>::PPW;
+#if PHT_TRACKW_RTREG
+    PointLog<N, false> pl; // (rho, vartheta) of the slot's point in registers for the whole row
+    pl.template load<PPW>(W.rt, q);
+#else
     PointLog<N, true> pl;
     pl.base = &W.rt[0][q];
     pl.stride = PPW;
+#endif
     const double tau = W.tau[q];
     const int m = sm.mk[k];
     const double2 *rec = R + (size_t)k * RecW<N>::U;
