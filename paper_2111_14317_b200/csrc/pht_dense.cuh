@@ -54,6 +54,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K)); }
 
+#ifndef PHT_DENSE_MINB
+#define PHT_DENSE_MINB 3 // resident CTAs per SM k_dense is compiled for (register budget)
+#endif
 template <int N>
 struct DGeo {
     static constexpr int KP = (N + 2 + 3) & ~3; // stage-2 K (vars + tau/const) padded to 4
@@ -106,7 +109,7 @@ struct DenseSmem {
 };
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(DGeo<N>::WARPS * 32, 3) k_dense(const DevSys S, const DenseSys D, const Args A)
+__global__ void __launch_bounds__(DGeo<N>::WARPS * 32, PHT_DENSE_MINB) k_dense(const DevSys S, const DenseSys D, const Args A)
 {
     using G = DGeo<N>;
     constexpr int KP = G::KP, KS = G::KS, CT = G::CT, NMT = G::NMT, PTS = G::PTS;
