@@ -744,24 +744,34 @@ def main():
     if world > 1:
         dist.barrier()
     # three timed groups of e2e_steps host-buffer steps; the median group is reported (the host
-    # link's run-to-run spread is large: profiles/r01_bench*.json)
-    e2e_runs = []
-    for _ in range(3):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            g.pc_step_host(xe, te, de, 1, se, ne)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        te_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te_ms, op=dist.ReduceOp.MAX)
-        e2e_runs.append(float(te_ms.item()))
+    # link's run-to-run spread is large: profiles/r01_bench*.json).  The headline chains the
+    # steps with pht_pc_step_host_async (each batch's copy-in overlaps the previous batch's
+    # copy-out; pht_host_wait at the end of the group, inside the timed region); the synchronous
+    # per-call entry point (pipeline filled and drained per step) is reported beside it.
+    def e2e_group(asynchronous):
+        runs = []
+        for _ in range(3):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.e2e_steps):
+                g.pc_step_host(xe, te, de, 1, se, ne, asynchronous=asynchronous)
+            if asynchronous:
+                g.host_wait()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            te_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(te_ms, op=dist.ReduceOp.MAX)
+            runs.append(float(te_ms.item()))
+        return runs
+    e2e_runs = e2e_group(True)
+    e2e_sync_runs = e2e_group(False)
     e2e_value = 2.0 * Pn * world * args.e2e_steps / (float(np.median(e2e_runs)) * 1e-3)
+    e2e_sync_value = 2.0 * Pn * world * args.e2e_steps / (float(np.median(e2e_sync_runs)) * 1e-3)
     link = host_link_bound(dev, Pn * (16 * N_VARS + 16), Pn * (16 * N_VARS + 8 + 1 + 8))
 
     peak_mhz = (clk.summary() or {}).get("sm_max_mhz") or 1965.0
@@ -798,6 +808,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pn * (16 * N_VARS + 16),
                     "d2h_bytes_per_step": Pn * (16 * N_VARS + 8 + 1 + 8),
                     "runs_ms": e2e_runs, "steps_per_run": args.e2e_steps,
+                    "entry_point": "pht_pc_step_host_async x steps_per_run + pht_host_wait (chained batches)",
+                    "per_call_sync": {"value": e2e_sync_value, "runs_ms": e2e_sync_runs,
+                                      "entry_point": "pht_pc_step_host (synchronous per call)"},
                     # the host link bounds this number: the step's copy-in and copy-out bytes moved
                     # concurrently (pinned, two streams, no kernel) take link_ms
                     "link_ms_per_step": link, "frac_of_link_bound":

@@ -276,6 +276,24 @@ int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
                      double *dn_norm, void *stream);
 
 /*
+ * pht_pc_step_host without the final synchronisation: returns once the pipeline is enqueued.
+ * The host buffers x, tau, dtau, status, dn_norm belong to the copy engines until
+ * pht_host_wait(sys, stream) returns (do not read or write them before).  Consecutive calls on one
+ * handle chain through the handle's internal streams: chunk c of a call starts copying in as soon
+ * as the previous call's chunk c has been copied out (same p; in-place x, tau), so one batch's
+ * copy-in overlaps the previous batch's kernels and copy-out instead of the whole pipeline
+ * filling and draining per call.  Orders itself after the work already submitted to `stream`.
+ * Results are identical to pht_pc_step_host.  Errors as pht_pc_step_host.
+ */
+int pht_pc_step_host_async(const pht_system *sys, int64_t p, double *x, double *tau,
+                           const double *dtau, int32_t newton_iters, uint8_t *status,
+                           double *dn_norm, void *stream);
+
+/* Orders `stream` after every host step of this handle submitted so far and synchronises it
+ * (the end of pht_pc_step_host_async chains).  PHT_OK when there was none. */
+int pht_host_wait(const pht_system *sys, void *stream);
+
+/*
  * Adaptive path tracking tau0 -> 0 on the device (step control = DESIGN.md
  * reading R14, the same algorithm as the oracle's tracker).  One persistent kernel: each slot
  * of each CTA runs one path (Euler predictor from dx/dtau, up to newton_iters Newton

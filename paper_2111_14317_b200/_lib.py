@@ -38,6 +38,8 @@ SIGNATURES = {
     "pht_euler_newton": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_pc_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "pht_pc_step_host": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "pht_pc_step_host_async": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "pht_host_wait": (ctypes.c_int, [_vp, _vp]),
     "pht_track_opts_default": (None, [ctypes.c_void_p]),
     "pht_track": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pht_track_cells": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),

@@ -177,9 +177,11 @@ class System:
         return st, dn
 
     def pc_step_host(self, x: np.ndarray, tau: np.ndarray, dtau: np.ndarray, newton_iters: int = 1,
-                     status: np.ndarray = None, dn_norm: np.ndarray = None):
+                     status: np.ndarray = None, dn_norm: np.ndarray = None, asynchronous: bool = False):
         """pht_pc_step_host on host numpy buffers (x, tau updated in place; pass pinned buffers,
-        including status/dn_norm, for copy/compute overlap)."""
+        including status/dn_norm, for copy/compute overlap).  asynchronous=True calls
+        pht_pc_step_host_async: the buffers (pass status/dn_norm to own them) are in flight until
+        host_wait(); consecutive calls overlap."""
         def host(a, dt, shape, what):
             if not (isinstance(a, np.ndarray) and a.dtype == dt and a.shape == shape and a.flags.c_contiguous):
                 raise PhtError(f"{what} must be a C-contiguous numpy {np.dtype(dt).name} array of shape {shape}")
@@ -194,12 +196,18 @@ class System:
         dn = host(dn_norm, np.float64, (p,), "dn_norm") if dn_norm is not None else np.empty(p, np.float64)
         if not x.flags.writeable or not tau.flags.writeable:
             raise PhtError("x and tau are updated in place: they must be writeable")
+        if asynchronous and (status is None or dn_norm is None):
+            raise PhtError("asynchronous host steps need caller-owned status and dn_norm buffers")
         d = self._dev()
-        check(self._lib.pht_pc_step_host(self._h, p, x.ctypes.data_as(ctypes.c_void_p),
-                                         tau.ctypes.data_as(ctypes.c_void_p), dtau.ctypes.data_as(ctypes.c_void_p),
-                                         int(newton_iters), st.ctypes.data_as(ctypes.c_void_p),
-                                         dn.ctypes.data_as(ctypes.c_void_p), _stream(d)), "pht_pc_step_host")
+        fn = self._lib.pht_pc_step_host_async if asynchronous else self._lib.pht_pc_step_host
+        check(fn(self._h, p, x.ctypes.data_as(ctypes.c_void_p), tau.ctypes.data_as(ctypes.c_void_p),
+                 dtau.ctypes.data_as(ctypes.c_void_p), int(newton_iters), st.ctypes.data_as(ctypes.c_void_p),
+                 dn.ctypes.data_as(ctypes.c_void_p), _stream(d)), "pht_pc_step_host")
         return st, dn
+
+    def host_wait(self):
+        """pht_host_wait: the current stream waits for (and synchronises with) every host step."""
+        check(self._lib.pht_host_wait(self._h, _stream(self._dev())), "pht_host_wait")
 
     def track(self, x, tau, stats: bool = True, **opts):
         """Adaptive tracking tau0 -> 0 in place (pht_track).  x: complex128 [p, n] start points,

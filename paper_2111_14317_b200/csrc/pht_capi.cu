@@ -112,8 +112,11 @@ struct pht_system {
     std::mutex ws_mu;
     // (copy-in, two compute, copy-out; per-chunk events: copy-in done, kernel done)
     cudaStream_t hs[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t hev_in[64] = {}, hev_k[64] = {};
+    cudaEvent_t hev_in[64] = {}, hev_k[64] = {}, hev_out[64] = {};
     cudaEvent_t hev0 = nullptr, hev_end = nullptr;
+    // the previous host step (pht_pc_step_host_async chains): its point count and chunk count
+    int64_t hprev_p = -1;
+    int hprev_nch = 0;
     int64_t ws_cap = 0;
     void *ws = nullptr;
 };
@@ -451,6 +454,7 @@ extern "C" void pht_system_destroy(pht_system *s)
     for (int c = 0; c < 64; ++c) {
         if (s->hev_in[c]) cudaEventDestroy(s->hev_in[c]);
         if (s->hev_k[c]) cudaEventDestroy(s->hev_k[c]);
+        if (s->hev_out[c]) cudaEventDestroy(s->hev_out[c]);
     }
     if (s->hev0) cudaEventDestroy(s->hev0);
     if (s->hev_end) cudaEventDestroy(s->hev_end);
@@ -788,6 +792,7 @@ static int ensure_streams(pht_system *s)
     for (int c = 0; c < 64; ++c) {
         cudaError_t e = cudaEventCreateWithFlags(&s->hev_in[c], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->hev_k[c], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->hev_out[c], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e);
     }
     cudaError_t e = cudaEventCreateWithFlags(&s->hev0, cudaEventDisableTiming);
@@ -795,8 +800,8 @@ static int ensure_streams(pht_system *s)
     return e == cudaSuccess ? PHT_OK : cuda_fail(e);
 }
 
-extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, double *tau, const double *dtau,
-                                int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
+static int host_step(const pht_system *cs, int64_t p, double *x, double *tau, const double *dtau, int32_t newton_iters,
+                     uint8_t *status, double *dn_norm, void *stream, bool async)
 {
     pht_system *s = const_cast<pht_system *>(cs);
     if (!s || p < 0 || newton_iters < 0 || (p > 0 && (!x || !tau || !dtau))) return PHT_EINVAL;
@@ -810,6 +815,7 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
     const size_t need = bx + 3 * bt + bs + 64;
     cudaError_t e;
     if ((int64_t)need > s->ws_cap) {
+        if (s->hs[3] && (e = cudaStreamSynchronize(s->hs[3])) != cudaSuccess) return cuda_fail(e); // in-flight async steps
         cudaFree(s->ws);
         s->ws = nullptr;
         s->ws_cap = 0;
@@ -832,9 +838,16 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
     // pipeline fill (first copy-in) and drain (last copy-out) are one chunk each
     int64_t chunk = (p + PHT_HOST_CHUNKS - 1) / PHT_HOST_CHUNKS;
     if (chunk < 32768) chunk = 32768;
+    const int nch = (int)((p + chunk - 1) / chunk);
+    // a previous host step may still be in flight (pht_pc_step_host_async): chunk c's copy-in
+    // overwrites the workspace range (and the host x / tau) that step's chunk c copies out, so it
+    // waits for that copy-out; a different point count (other chunking) waits for the whole step
+    const bool chain = s->hprev_p == p && s->hprev_nch == nch;
+    if (s->hprev_p >= 0 && !chain && (e = cudaStreamWaitEvent(sin, s->hev_end, 0)) != cudaSuccess) return cuda_fail(e);
     int c = 0;
     for (int64_t b = 0; b < p; b += chunk, ++c) {
         const int64_t m = (p - b < chunk) ? p - b : chunk;
+        if (chain && (e = cudaStreamWaitEvent(sin, s->hev_out[c], 0)) != cudaSuccess) return cuda_fail(e);
         const size_t ox = (size_t)b * n * 2, mx = (size_t)m * n * 16, mt = (size_t)m * 8;
         cudaStream_t sk = s->hs[1 + (c & 1)];
         if ((e = cudaMemcpyAsync(dx + ox, x + ox, mx, cudaMemcpyHostToDevice, sin)) != cudaSuccess ||
@@ -850,12 +863,44 @@ extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, doub
             (e = cudaMemcpyAsync(x + ox, dx + ox, mx, cudaMemcpyDeviceToHost, sout)) != cudaSuccess ||
             (e = cudaMemcpyAsync(tau + b, dtu + b, mt, cudaMemcpyDeviceToHost, sout)) != cudaSuccess ||
             (status && (e = cudaMemcpyAsync(status + b, dst + b, (size_t)m, cudaMemcpyDeviceToHost, sout)) != cudaSuccess) ||
-            (dn_norm && (e = cudaMemcpyAsync(dn_norm + b, ddn + b, mt, cudaMemcpyDeviceToHost, sout)) != cudaSuccess))
+            (dn_norm && (e = cudaMemcpyAsync(dn_norm + b, ddn + b, mt, cudaMemcpyDeviceToHost, sout)) != cudaSuccess) ||
+            (e = cudaEventRecord(s->hev_out[c], sout)) != cudaSuccess)
             return cuda_fail(e);
     }
+    s->hprev_p = p;
+    s->hprev_nch = nch;
     // every chunk's copy-out is on sout, after its kernel; the caller's stream waits for the last
-    if ((e = cudaEventRecord(s->hev_end, sout)) != cudaSuccess || (e = cudaStreamWaitEvent(st, s->hev_end, 0)) != cudaSuccess)
-        return cuda_fail(e);
+    // (the asynchronous variant leaves that to pht_host_wait)
+    if ((e = cudaEventRecord(s->hev_end, sout)) != cudaSuccess) return cuda_fail(e);
+    if (async) return PHT_OK;
+    if ((e = cudaStreamWaitEvent(st, s->hev_end, 0)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
+    return PHT_OK;
+}
+
+extern "C" int pht_pc_step_host(const pht_system *cs, int64_t p, double *x, double *tau, const double *dtau,
+                                int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
+{
+    return host_step(cs, p, x, tau, dtau, newton_iters, status, dn_norm, stream, false);
+}
+
+extern "C" int pht_pc_step_host_async(const pht_system *cs, int64_t p, double *x, double *tau, const double *dtau,
+                                      int32_t newton_iters, uint8_t *status, double *dn_norm, void *stream)
+{
+    return host_step(cs, p, x, tau, dtau, newton_iters, status, dn_norm, stream, true);
+}
+
+extern "C" int pht_host_wait(const pht_system *cs, void *stream)
+{
+    pht_system *s = const_cast<pht_system *>(cs);
+    if (!s) return PHT_EINVAL;
+    std::lock_guard<std::mutex> lk(s->ws_mu);
+    if (!s->hs[0] || s->hprev_p < 0) return PHT_OK; // no host step yet
+    DevGuard g(s->device);
+    if (!g.ok) return cuda_fail(cudaGetLastError());
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaStreamWaitEvent(st, s->hev_end, 0)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
     return PHT_OK;
 }

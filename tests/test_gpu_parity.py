@@ -267,6 +267,41 @@ def test_pc_step_host_equals_device(P, p):
     assert np.array_equal(xp.numpy(), xh) and np.array_equal(tp.numpy(), th)
 
 
+def test_pc_step_host_async_chain_equals_sync(P):
+    """pht_pc_step_host_async: three chained steps (each chunk's copy-in waits only for the
+    previous step's copy-out of the same chunk), then one with a different point count (waits for
+    the whole chain), then pht_host_wait -- bitwise the results of the synchronous calls, and a
+    synchronous call after an async chain orders itself behind it."""
+    sysm = W.cyclic(10, lift_max=100)
+    g = P.System.from_workload(sysm)
+    p = 300_007                                    # 10 chunks of 32,768 (the minimum), the last one ragged
+    x, _, tau = W.random_points(p, 10, seed=17)
+    dtau = np.full(p, 0.01)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    xs, ts = x.copy(), tau.copy()
+    for _ in range(3):
+        g.pc_step_host(xs, ts, dtau)
+    xa, ta, da = pin(x), pin(tau), pin(dtau)
+    sa, na = pin(np.zeros(p, np.uint8)), pin(np.zeros(p))
+    for _ in range(3):
+        g.pc_step_host(xa, ta, da, 1, sa, na, asynchronous=True)
+    q = 70_001
+    xq, tq, dq = pin(x[:q]), pin(tau[:q]), pin(dtau[:q])
+    sq, nq = pin(np.zeros(q, np.uint8)), pin(np.zeros(q))
+    g.pc_step_host(xq, tq, dq, 1, sq, nq, asynchronous=True)
+    g.host_wait()
+    assert np.array_equal(xa, xs) and np.array_equal(ta, ts)
+    x1, t1 = x[:q].copy(), tau[:q].copy()
+    g.pc_step_host(x1, t1, dtau[:q])
+    assert np.array_equal(xq, x1) and np.array_equal(tq, t1)
+    g.pc_step_host(xa, ta, da, 1, sa, na, asynchronous=True)
+    xs2, ts2 = xs.copy(), ts.copy()
+    g.pc_step_host(xs2, ts2, dtau)                 # a synchronous step right behind an async one
+    g.host_wait()
+    g.pc_step_host(xs, ts, dtau)
+    assert np.array_equal(xa, xs) and np.array_equal(xs2, xs)
+
+
 def test_evaluate_vanishing_terms_huge_lifting(P):
     """A term with tau*omega ~ -1e7 (far below the row) must vanish, not wrap the exponent:
     h = x1 - t^(10^7) x2 at tau = -1 equals x1 (regression: 32-bit overflow in the exp reduction)."""
