@@ -383,7 +383,7 @@ const char *pht_strerror(int code);
 const char *pht_last_cuda_error(void);
 
 /* ABI version (incremented on any signature change). */
-int pht_version(void); /* 3: pht_track_opts.reuse_tangent; 2: pht_system_set_kernels, PHT_PT_FLOOR */
+int pht_version(void); /* 4: pht_pc_step_host_async, pht_host_wait; 3: pht_track_opts.reuse_tangent; 2: pht_system_set_kernels, PHT_PT_FLOOR */
 
 #ifdef __cplusplus
 }

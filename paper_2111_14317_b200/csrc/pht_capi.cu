@@ -1080,4 +1080,4 @@ extern "C" const char *pht_strerror(int code)
     }
 }
 
-extern "C" int pht_version(void) { return 3; }
+extern "C" int pht_version(void) { return 4; }

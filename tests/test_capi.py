@@ -32,7 +32,7 @@ def test_binding_covers_header():
 def test_version_and_strerror_without_gpu():
     from paper_2111_14317_b200 import _lib
     lib = _lib.load()
-    assert lib.pht_version() == 3
+    assert lib.pht_version() == 4
     assert lib.pht_strerror(-3).decode().startswith("duplicate")
     assert lib.pht_launch_count() >= 0
 
