@@ -2258,12 +2258,16 @@ struct SmemTW {
 #ifndef PHT_TRACKW_RTREG
 #define PHT_TRACKW_RTREG 0 // experiments: (rho, vartheta) held in registers through the row loop
 #endif
+// LPR = 3 is the balanced mode (trackw_lanes): row k owns gk = 2 or 3 consecutive lanes from lane
+// gbase, lane h of them takes the terms h, h + gk, ...
 template <int N, int LPR, bool COMP = false>
 __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const double2 *R, const TrackW<N, LPR> &W,
                                             int k, int q, int h, const double *wq, double2 (&row)[N + 2], int &e,
-                                            unsigned mask = 0xffffffffu) // lanes executing this call (LPR shuffles)
+                                            unsigned mask = 0xffffffffu, // lanes executing this call (LPR shuffles)
+                                            int gk = LPR, int gbase = 0)
 {
     constexpr int RS = rec_stride(N), PPW = GeoTW<N, LPR>::PPW;
+    const int step = (LPR == 3) ? gk : LPR; // term stride of this lane
 #if PHT_TRACKW_RTREG
     PointLog<N, false> pl; // (rho, vartheta) of the slot's point in registers for the whole row
     pl.template load<PPW>(W.rt, q);
@@ -2289,7 +2293,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
     }
     int i = h;
     if (COMP) {
-        for (; i < m; i += LPR) {
+        for (; i < m; i += step) {
             double a[RS];
             load_rec_s<N>(rec + (size_t)i * TS, a);
             if (wk) a[N] = __ldg(wk + i);
@@ -2318,7 +2322,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
         acc.add(a, wa);
         acc.add(b, wb);
     }
-    for (; i < m; i += LPR) {
+    for (; i < m; i += step) {
         double a[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
         if (wk) a[N] = __ldg(wk + i);
@@ -2332,6 +2336,26 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
     row[N] = acc.gt;
     row[N + 1] = acc.h;
     double ed = acc.ed;
+    if (LPR == 3) {
+        // balanced mode: every lane of the group forms the same sum in the same order (lane
+        // gbase + 0, + 1, + 2), each partial row first aligned to the group's largest exponent
+        const int s1 = gbase + 1, s2 = gbase + (gk == 3 ? 2 : 1);
+        const double e0 = __shfl_sync(mask, ed, gbase), e1 = __shfl_sync(mask, ed, s1),
+                     e2 = __shfl_sync(mask, ed, s2);
+        const double em = fmax(fmax(e0, e1), e2);
+        const int d = (int)fmax(ed - em, -2000.0), d1 = d / 2;
+        const double f1 = scalbn(1.0, d1), f2 = scalbn(1.0, d - d1);
+#pragma unroll
+        for (int c = 0; c < N + 2; ++c) {
+            const double2 v = make_double2(row[c].x * f1 * f2, row[c].y * f1 * f2);
+            const double x0 = __shfl_sync(mask, v.x, gbase), y0 = __shfl_sync(mask, v.y, gbase);
+            const double x1 = __shfl_sync(mask, v.x, s1), y1 = __shfl_sync(mask, v.y, s1);
+            const double x2 = __shfl_sync(mask, v.x, s2), y2 = __shfl_sync(mask, v.y, s2);
+            row[c] = gk == 3 ? make_double2((x0 + x1) + x2, (y0 + y1) + y2) : make_double2(x0 + x1, y0 + y1);
+        }
+        e = (int)em;
+        return;
+    }
 #pragma unroll
     for (int off = 1; off < LPR; off <<= 1) {
         // align to the larger row exponent (two normal power-of-two factors, see RowAcc::reduce),
@@ -2369,9 +2393,34 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
     if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
     if (tid <= N) sm.off[tid] = __ldg(S.off + tid);
     TrackW<N, LPR> &W = sm.w[wi];
-    // lane = (i * PPW + q) * LPR + h: row / variable i of slot q, term share h of that row
-    const bool inseg = lane < N * PPW * LPR;
-    const int gl = lane / LPR, h = lane % LPR;
+    // lane = (i * PPW + q) * LPR + h: row / variable i of slot q, term share h of that row;
+    // balanced mode (LPR = 3, one slot): row i owns gi = 3 lanes if it is among the 32 - 2N rows
+    // with the most terms, else 2 (ties: lower index first), the rows' groups in index order
+    int gi = LPR, gbase = 0, ibal = 0, hbal = 0, used = N * PPW * LPR;
+    if (LPR == 3) {
+        int mk_[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) mk_[j] = __ldg(S.off + j + 1) - __ldg(S.off + j);
+        const int n3 = min(N, 32 - 2 * N);
+        int b = 0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            int rank = 0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) rank += (mk_[l] > mk_[j] || (mk_[l] == mk_[j] && l < j)) ? 1 : 0;
+            const int g = rank < n3 ? 3 : 2;
+            if (lane >= b && lane < b + g) {
+                ibal = j;
+                hbal = lane - b;
+                gi = g;
+                gbase = b;
+            }
+            b += g;
+        }
+        used = b;
+    }
+    const bool inseg = lane < used;
+    const int gl = LPR == 3 ? ibal : lane / LPR, h = LPR == 3 ? hbal : lane % LPR;
     const int q = inseg ? gl % PPW : 0, i = inseg ? gl / PPW : 0;
     const int seg0 = inseg ? q : PPW;
     const bool prim = inseg && h == 0; // the lane that owns row / variable i of slot q
@@ -2442,13 +2491,13 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             const bool fin = W.phase[q] == PH_FINAL;
             const unsigned bal = __ballot_sync(0xffffffffu, fin);
             if (bal == 0u)
-                eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e);
+                eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e, 0xffffffffu, gi, gbase);
             else if (bal == 0xffffffffu)
-                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e);
+                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e, 0xffffffffu, gi, gbase);
             else if (fin)
-                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e, bal);
+                eval_row_tw<N, LPR, true>(sm, R, W, i, q, h, wq, a, e, bal, gi, gbase);
             else
-                eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e, ~bal);
+                eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e, ~bal, gi, gbase);
             __syncwarp();
             normalize_row<N>(a);
             int col;
@@ -2533,8 +2582,11 @@ cudaError_t launch_trackw_l(const DevSys &S, const TrackArgs &A, cudaStream_t st
 // Lanes per row of k_trackw: when every path gets its own slot in one wave with LPR = 2 (or 4)
 // lanes per row, the per-iteration latency of the row loop (the time to the last path at small
 // path counts, katsura-10: 990 paths) shrinks; otherwise one lane per row (throughput).
+#ifndef PHT_TRACKW_BALANCED
+#define PHT_TRACKW_BALANCED 1 // few paths and n >= 9: 2-3 lanes per row over the whole warp (LPR = 3)
+#endif
 #ifndef PHT_TRACKW_LPR
-#define PHT_TRACKW_LPR 0 // 0: automatic; 1, 2, 4: forced (experiments)
+#define PHT_TRACKW_LPR 0 // 0: automatic; 1, 2, 3 (balanced), 4: forced (experiments)
 #endif
 template <int N, bool LOGS>
 cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
@@ -2548,6 +2600,10 @@ cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t st
         else if (N * 2 <= 32 && (A.P + GeoTW<N, 2>::PPW - 1) / GeoTW<N, 2>::PPW <= sms * slots_per_sm) lpr = 2;
     }
     if (lpr == 4 && N * 4 <= 32) return launch_trackw_l<N, LOGS, (N * 4 <= 32 ? 4 : 1)>(S, A, stream, sms);
+    // n >= 9 (no LPR = 4): the balanced mode gives every row 2 or 3 lanes of the warp (katsura-10,
+    // n = 11: 10 rows x 3 + 1 x 2 = 32 lanes, at most 4 terms per lane instead of 6)
+    if ((lpr == 3 || (lpr == 2 && PHT_TRACKW_BALANCED)) && N * 2 <= 32 && N * 4 > 32)
+        return launch_trackw_l<N, LOGS, (N * 2 <= 32 ? 3 : 1)>(S, A, stream, sms);
     if (lpr >= 2 && N * 2 <= 32) return launch_trackw_l<N, LOGS, (N * 2 <= 32 ? 2 : 1)>(S, A, stream, sms);
     return launch_trackw_l<N, LOGS, 1>(S, A, stream, sms);
 }
