@@ -2336,7 +2336,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
     row[N] = acc.gt;
     row[N + 1] = acc.h;
     double ed = acc.ed;
-    if (LPR == 3) {
+    if constexpr (LPR == 3) {
         // balanced mode: every lane of the group forms the same sum in the same order (lane
         // gbase + 0, + 1, + 2), each partial row first aligned to the group's largest exponent
         const int s1 = gbase + 1, s2 = gbase + (gk == 3 ? 2 : 1);
@@ -2354,8 +2354,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
             row[c] = gk == 3 ? make_double2((x0 + x1) + x2, (y0 + y1) + y2) : make_double2(x0 + x1, y0 + y1);
         }
         e = (int)em;
-        return;
-    }
+    } else {
 #pragma unroll
     for (int off = 1; off < LPR; off <<= 1) {
         // align to the larger row exponent (two normal power-of-two factors, see RowAcc::reduce),
@@ -2372,6 +2371,7 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
         ed = em;
     }
     e = (int)ed;
+    }
 }
 
 template <int N, bool LOGS, int LPR>
