@@ -2374,7 +2374,9 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
     }
 }
 
-template <int N, bool LOGS, int LPR>
+// PROJ: projective systems (x state, LPR = 1): the bordering row and the unit-sphere renormalisation,
+// compiled in only where used (the checks cost the affine kernels ~8% when present at run time)
+template <int N, bool LOGS, int LPR, bool PROJ = false>
 __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(const DevSys S, const TrackArgs A, int MT)
 {
     using G = GeoW<N>;
@@ -2385,13 +2387,16 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     const TrackOpts &o = A.o;
     load_tables(S, sm.exptab, sm.cistab, tid, G::NT);
+    // a projective system has N - 1 polynomial rows; row N - 1 is the bordering row y^* (no terms)
+    const int NE = PROJ ? N - 1 : N;
     for (int idx = tid; idx < MT * N; idx += G::NT) { // records, term-major (only t < m_k is read)
         const int kk = idx % N, t = idx / N;
+        if (kk >= NE) continue;
         const int i0 = __ldg(S.off + kk), m = __ldg(S.off + kk + 1) - i0;
         if (t < m) pack_rec_w<N>(S.rec + (size_t)(i0 + t) * (RS / 2), R + (size_t)idx * RecW<N>::U);
     }
-    if (tid < N) sm.mk[tid] = __ldg(S.off + tid + 1) - __ldg(S.off + tid);
-    if (tid <= N) sm.off[tid] = __ldg(S.off + tid);
+    if (tid < N) sm.mk[tid] = tid < NE ? __ldg(S.off + tid + 1) - __ldg(S.off + tid) : 0;
+    if (tid <= N) sm.off[tid] = __ldg(S.off + (tid < NE ? tid : NE));
     TrackW<N, LPR> &W = sm.w[wi];
     // lane = (i * PPW + q) * LPR + h: row / variable i of slot q, term share h of that row;
     // balanced mode (LPR = 3, one slot): row i owns gi = 3 lanes if it is among the 32 - 2N rows
@@ -2449,6 +2454,11 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             else if (ph != PH_IDLE) xv = W.xa[i][q];
         }
         __syncwarp();
+        if (PROJ) { // a new projective path goes onto ||y|| = 1 first (reading R29)
+            if (lane < PPW && W.refill[lane]) proj_normalize<N>(W.xa, lane);
+            __syncwarp();
+            if (prim && W.phase[q] != PH_CORRECT && W.phase[q] != PH_IDLE) xv = W.xa[i][q];
+        }
         if (lane < PPW) {
             W.done_path[lane] = -1;
             W.acc[lane] = 0;
@@ -2499,6 +2509,12 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             else
                 eval_row_tw<N, LPR, false>(sm, R, W, i, q, h, wq, a, e, ~bal, gi, gbase);
             __syncwarp();
+            if (PROJ && i == N - 1) { // bordering row y^* (P:237-252): y^* (y (.) delta) = sum |y_j|^2 delta_j
+#pragma unroll
+                for (int j = 0; j < N; ++j) a[j] = make_double2(exp(2.0 * W.rt[j][q].x), 0.0);
+                a[N] = a[N + 1] = make_double2(0.0, 0.0);
+                e = 0;
+            }
             normalize_row<N>(a);
             int col;
             double2 dE, dN;
@@ -2525,15 +2541,23 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
                 } else if (ph == PH_CORRECT) {
                     const double2 v = W.xt[i][q];
                     W.xt[i][q] = trk_update<N, LOGS>(v, dl, 1.0, S);
-                    W.nd2[i][q] = fma(dl.x, dl.x, dl.y * dl.y); // |dx_i / x_i|^2 (reading R14)
+                    // |dx_i / x_i|^2 (reading R14); projective: |dy_i|^2 with ||y|| = 1 (R29)
+                    const double r2 = fma(dl.x, dl.x, dl.y * dl.y);
+                    W.nd2[i][q] = PROJ ? r2 * fma(v.x, v.x, v.y * v.y) : r2;
                 } else { // FINAL
                     const double2 v = W.xa[i][q];
                     W.xa[i][q] = trk_update<N, LOGS>(v, dl, 1.0, S);
-                    W.nd2[i][q] = fma(dl.x, dl.x, dl.y * dl.y);
+                    const double r2 = fma(dl.x, dl.x, dl.y * dl.y);
+                    W.nd2[i][q] = PROJ ? r2 * fma(v.x, v.x, v.y * v.y) : r2;
                 }
             }
         }
         __syncwarp();
+        if (PROJ) { // updated points back onto ||y|| = 1 (x state only, reading R29)
+            if (lane < PPW && W.st[lane] == 0 && W.phase[lane] != PH_IDLE)
+                proj_normalize<N>(W.phase[lane] == PH_FINAL ? W.xa : W.xt, lane);
+            __syncwarp();
+        }
         // (4) per-slot decisions
         if (lane < PPW && W.phase[lane] != PH_IDLE) trk_decide<N, LOGS>(W, A, S, lane, W.st[lane]);
         __syncwarp();
@@ -2547,14 +2571,14 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
 }
 
 #ifndef __CUDACC_RTC__
-// k_trackw: n <= 12, LU, affine systems, Euler predictor; PHT_TRACKW=0 selects k_track.
+// k_trackw: n <= 12, LU, affine or projective systems, Euler predictor; PHT_TRACKW=0 selects k_track.
 template <int N>
 bool trackw_eligible(const DevSys &S, const TrackArgs &A)
 {
-    return N <= 12 && !S.proj && A.solver == SOLVER_LU && A.o.predictor != 1 && S.mt > 0;
+    return N <= 12 && A.solver == SOLVER_LU && A.o.predictor != 1 && S.mt > 0; // projective: LPR = 1
 }
 
-template <int N, bool LOGS, int LPR>
+template <int N, bool LOGS, int LPR, bool PROJ = false>
 cudaError_t launch_trackw_l(const DevSys &S, const TrackArgs &A, cudaStream_t stream, int sms)
 {
     constexpr int PPW = GeoTW<N, LPR>::PPW;
@@ -2564,18 +2588,18 @@ cudaError_t launch_trackw_l(const DevSys &S, const TrackArgs &A, cudaStream_t st
     int dev = 0;
     cudaGetDevice(&dev);
     if ((int64_t)sb > conf_sb[dev & 63].load()) {
-        cudaError_t e = cudaFuncSetAttribute(k_trackw<N, LOGS, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+        cudaError_t e = cudaFuncSetAttribute(k_trackw<N, LOGS, LPR, PROJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
         if (e != cudaSuccess) return e;
         conf_sb[dev & 63].store((int64_t)sb);
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trackw<N, LOGS, LPR>, GeoW<N>::NT, sb);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trackw<N, LOGS, LPR, PROJ>, GeoW<N>::NT, sb);
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)sms * per_sm;
     const int64_t need = (A.P + (int64_t)PPW * GeoW<N>::WARPS - 1) / ((int64_t)PPW * GeoW<N>::WARPS);
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    k_trackw<N, LOGS, LPR><<<dim3((unsigned)grid), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
+    k_trackw<N, LOGS, LPR, PROJ><<<dim3((unsigned)grid), dim3(GeoW<N>::NT), sb, stream>>>(S, A, S.mt);
     return cudaGetLastError();
 }
 
@@ -2593,6 +2617,10 @@ cudaError_t launch_trackw_t(const DevSys &S, const TrackArgs &A, cudaStream_t st
 {
     // warps resident per SM of the LPR > 1 kernels (their register budget: GeoTW::MINB)
     const int64_t slots_per_sm = (int64_t)GeoW<N>::WARPS * GeoTW<N, 2>::MINB;
+    if (S.proj) { // projective systems (x state only): one lane per row
+        if constexpr (!LOGS) return launch_trackw_l<N, false, 1, true>(S, A, stream, sms);
+        return cudaErrorNotSupported;
+    }
     int lpr = PHT_TRACKW_LPR;
     if (lpr == 0) {
         lpr = 1;
