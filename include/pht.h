@@ -283,7 +283,8 @@ int pht_pc_step_host(const pht_system *sys, int64_t p, double *x, double *tau,
  * as the previous call's chunk c has been copied out (same p; in-place x, tau), so one batch's
  * copy-in overlaps the previous batch's kernels and copy-out instead of the whole pipeline
  * filling and draining per call.  Orders itself after the work already submitted to `stream`.
- * Results are identical to pht_pc_step_host.  Errors as pht_pc_step_host.
+ * Results are identical to pht_pc_step_host.  Errors as pht_pc_step_host.  pht_system_destroy
+ * waits for host steps still in flight.
  */
 int pht_pc_step_host_async(const pht_system *sys, int64_t p, double *x, double *tau,
                            const double *dtau, int32_t newton_iters, uint8_t *status,

@@ -438,6 +438,10 @@ extern "C" void pht_system_destroy(pht_system *s)
 {
     if (!s) return;
     DevGuard g(s->device);
+    // host steps still in flight (pht_pc_step_host_async without pht_host_wait) finish first:
+    // their copies use the workspace, the events and the streams released below
+    for (int u = 0; u < 4; ++u)
+        if (s->hs[u]) cudaStreamSynchronize(s->hs[u]);
     cudaFree(s->d_rec);
     cudaFree(s->d_off);
     cudaFree(s->d_exptab);
