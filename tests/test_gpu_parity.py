@@ -302,6 +302,25 @@ def test_pc_step_host_async_chain_equals_sync(P):
     assert np.array_equal(xa, xs) and np.array_equal(xs2, xs)
 
 
+def test_destroy_waits_for_async_host_steps(P):
+    """pht_system_destroy right after pht_pc_step_host_async (no pht_host_wait): the handle waits
+    for the in-flight copies before it releases the workspace, events and streams; the host
+    buffers hold the finished step afterwards."""
+    sysm = W.cyclic(10, lift_max=100)
+    p = 200_000
+    x, _, tau = W.random_points(p, 10, seed=19)
+    dtau = np.full(p, 0.01)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    xa, ta, da = pin(x), pin(tau), pin(dtau)
+    sa, na = pin(np.zeros(p, np.uint8)), pin(np.zeros(p))
+    g = P.System.from_workload(sysm)
+    g.pc_step_host(xa, ta, da, 1, sa, na, asynchronous=True)
+    g.close()
+    xs, ts = x.copy(), tau.copy()
+    P.System.from_workload(sysm).pc_step_host(xs, ts, dtau)
+    assert np.array_equal(xa, xs) and np.array_equal(ta, ts)
+
+
 def test_evaluate_vanishing_terms_huge_lifting(P):
     """A term with tau*omega ~ -1e7 (far below the row) must vanish, not wrap the exponent:
     h = x1 - t^(10^7) x2 at tau = -1 equals x1 (regression: 32-bit overflow in the exp reduction)."""
