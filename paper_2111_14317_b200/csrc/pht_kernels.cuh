@@ -2221,6 +2221,8 @@ struct GeoTW {
     // pivot-row broadcast by shuffles in the latency-bound few-path tracker (no shared round trip
     // and no __syncwarp per pivot), through shared memory in the throughput kernels
     static constexpr bool SHFL = LPR > 1 ? (bool)PHT_TRACKW_LOWOCC_SHFL : (bool)PHT_W_SHFL;
+    // the shuffle broadcast finds the pivot row's lane as (r PPW + q) LPR: not the balanced layout
+    static_assert(!(SHFL && LPR == 3), "balanced lanes (LPR = 3) broadcast the pivot row through shared memory");
 };
 
 template <int N, int LPR = 1>
