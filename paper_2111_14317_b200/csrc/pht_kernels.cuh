@@ -845,7 +845,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src)
     return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-template <int N, int PPW, int KS, bool IMAJ = false, int LPR = 1, bool SHFL = (bool)PHT_W_SHFL>
+template <int N, int PPW, int KS, bool IMAJ = false, int LPR = 1, bool SHFL = (bool)PHT_W_SHFL, bool DB = false>
 __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, unsigned *kseg, int seg0, int seg,
                                             int i, bool act, int &col, double2 &dE, double2 &dN, bool &singular,
                                             bool prim = true)
@@ -910,16 +910,20 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
         a[j] = me ? a[j] : make_double2(0.0, 0.0);
         if (PPW > 4) __syncwarp(); // kseg is rewritten by the next pivot search
         } else {
+        // DB: pivots alternate between two row buffers, so the barrier after the
+        // elimination goes (pivot j + 1's publish barrier orders pivot j's reads before pivot
+        // j + 2's writes); the caller then provides 2 (RW | 1) entries per point
+        double2 *pr = prow + (DB ? (j & 1) * (RW | 1) : 0);
         if (me && act && prim) {
             // the pivot row with the pivot replaced by its reciprocal (computed before the
             // argmax by every lane for its own candidate: the reciprocal's latency overlaps the
             // pivot search instead of following the row broadcast)
-            prow[j] = crcp;
+            pr[j] = crcp;
 #pragma unroll
-            for (int c = j + 1; c < RW; ++c) prow[c] = a[c];
+            for (int c = j + 1; c < RW; ++c) pr[c] = a[c];
         }
         __syncwarp();
-        const double2 rcp = prow[j];
+        const double2 rcp = pr[j];
         {
             // branch-free: pivot at or below the threshold, or too large for a normal |a_j|^2
             const double pa = cabs1(a[j]);
@@ -931,14 +935,14 @@ __device__ __forceinline__ void lsolve_regs(double2 (&a)[N + 2], double2 *prow, 
         double2 l = cmul(a[j], rcp);
         l = me ? make_double2(0.0, 0.0) : l;
 #pragma unroll
-        for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, prow[c]);
-        __syncwarp();
+        for (int c = j + 1; c < RW; ++c) a[c] = cfms(a[c], l, pr[c]);
+        if (!DB) __syncwarp();
         }
     }
     if (!SHFL) {
         // prow[c] (c < N) still holds the reciprocal of column c's pivot (later steps only write
         // prow[j'..] with j' > c): the lane's own pivot reciprocal without a select per pivot
-        myrcp = prow[col];
+        myrcp = prow[(DB ? (col & 1) * (RW | 1) : 0) + col]; // (written by this lane)
         __syncwarp(); // the caller may reuse prow
     }
     const double2 e = cmul(a[N], myrcp), n = cmul(a[N + 1], myrcp);
@@ -2210,6 +2214,9 @@ __global__ void __launch_bounds__(Geo<N>::NT, Geo<N>::MINB) k_track(const DevSys
 #ifndef PHT_TRACKW_LOWOCC_SHFL
 #define PHT_TRACKW_LOWOCC_SHFL 0 // measured: katsura-10 4.3 ms with shuffles vs 3.8 through shared memory
 #endif
+#ifndef PHT_TRACKW_LOWOCC_DB
+#define PHT_TRACKW_LOWOCC_DB 1 // LPR > 1: double-buffered pivot row, one warp barrier less per pivot (katsura-10 -3%)
+#endif
 #ifndef PHT_TRACKW_LOWOCC_PAIR
 #define PHT_TRACKW_LOWOCC_PAIR 0 // LPR > 1: two terms per iteration (ILP) for n <= 12
 #endif
@@ -2221,6 +2228,8 @@ struct GeoTW {
     // pivot-row broadcast by shuffles in the latency-bound few-path tracker (no shared round trip
     // and no __syncwarp per pivot), through shared memory in the throughput kernels
     static constexpr bool SHFL = LPR > 1 ? (bool)PHT_TRACKW_LOWOCC_SHFL : (bool)PHT_W_SHFL;
+    // double-buffered pivot row in the latency-bound few-path tracker
+    static constexpr bool DB = LPR > 1 && PHT_TRACKW_LOWOCC_DB;
     // the shuffle broadcast finds the pivot row's lane as (r PPW + q) LPR: not the balanced layout
     static_assert(!(SHFL && LPR == 3), "balanced lanes (LPR = 3) broadcast the pivot row through shared memory");
 };
@@ -2234,7 +2243,7 @@ struct TrackW {
     double2 ec[N][PPW];                 // Euler direction at the accepted point (re-prediction)
     double2 ecn[N][PPW];                // reuse_tangent: Euler direction at the latest corrector iterate
     double nd2[N][PPW];
-    double2 prow[PPW][GeoW<N>::RW | 1];
+    double2 prow[PPW][(1 + GeoTW<N, LPR>::DB) * (GeoW<N>::RW | 1)];
     alignas(16) unsigned keys[PPW * GeoW<N>::KS];
     double tau[PPW];                    // query tau
     double tau_a[PPW], tau_t[PPW], dt[PPW], prev[PPW], nd1[PPW], tau_p[PPW];
@@ -2521,7 +2530,7 @@ __global__ void __launch_bounds__(GeoW<N>::NT, (GeoTW<N, LPR>::MINB)) k_trackw(c
             int col;
             double2 dE, dN;
             bool sing;
-            lsolve_regs<N, PPW, G::KS, true, LPR, GeoTW<N, LPR>::SHFL>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q,
+            lsolve_regs<N, PPW, G::KS, true, LPR, GeoTW<N, LPR>::SHFL, GeoTW<N, LPR>::DB>(a, &W.prow[q][0], &W.keys[q * G::KS], seg0, q,
                                                                         i, inseg, col, dE, dN, sing, prim);
             if (prim) {
                 if (sing) atomicOr(&W.st[q], PT_SINGULAR);
