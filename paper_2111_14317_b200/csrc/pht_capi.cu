@@ -237,7 +237,6 @@ static int build_dense(pht_system *s)
     for (int k = 0; k < n; ++k) {
         const int m = off[k + 1] - off[k];
         if (m == 0) return PHT_EINVAL;
-        max_ntk = std::max(max_ntk, (m + 7) / 8);
         if (slot.size() % 8 != 0 && mid_start) // a second boundary in this tile: pad to the next tile
             while (slot.size() % 8 != 0) { slot.push_back(-1); slot_eq.push_back(k - 1); }
         mid_start = slot.size() % 8 != 0;
@@ -411,7 +410,7 @@ static int create_impl(int32_t n_eq, int32_t n_var, const int64_t *off, const in
     // (pht_system_set_kernels(PHT_KERNELS_DENSE))
     if (n >= 10 && !proj) {
         const int rc = build_dense(s);
-        if (rc != PHT_OK) {
+        if (rc != PHT_OK && rc != PHT_EUNSUPPORTED) { // (unsupported: > 65,535 n-tiles; no DMMA tables)
             pht_system_destroy(s);
             return rc;
         }
