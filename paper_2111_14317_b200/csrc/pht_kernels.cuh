@@ -2314,13 +2314,13 @@ __device__ __forceinline__ void eval_row_tw(const SmemTW<N, LPR> &sm, const doub
             acc.add(a, expcis<true>(acc.reduced2(ph, pl_), th, sm.exptab, sm.cistab, tl));
         }
     }
-    for (; GeoTW<N, LPR>::PAIR && i + LPR < m; i += 2 * LPR) {
+    for (; GeoTW<N, LPR>::PAIR && i + step < m; i += 2 * step) {
         double a[RS], b[RS];
         load_rec_s<N>(rec + (size_t)i * TS, a);
-        load_rec_s<N>(rec + (size_t)(i + LPR) * TS, b);
+        load_rec_s<N>(rec + (size_t)(i + step) * TS, b);
         if (wk) {
             a[N] = __ldg(wk + i);
-            b[N] = __ldg(wk + i + LPR);
+            b[N] = __ldg(wk + i + step);
         }
         double pa, pb, ta, tb;
         phi_theta<N>(a, pl, tau, pa, ta);
